@@ -1,0 +1,176 @@
+/* ragcache_b200.h — C-ABI of the B200-native RAGCache GPU hot path.
+ *
+ * The reference (ragsim, /root/reference/pkg/src/ragsim) is pure Python and
+ * has no FFI: its GPU work is modelled by three stand-ins, and every entry
+ * point below is the native operation that executes what the stand-in only
+ * accounts for.  The host-side decision logic (KnowledgeTree, PGDSF,
+ * ReorderQueue, DSP controller) stays in the reference's Python and calls
+ * these through ctypes.
+ *
+ * Conventions: plain pointers and sizes only; every call returns an int
+ * status.  Stream arguments are cudaStream_t passed as void* (NULL = legacy
+ * default stream).  Device pointers are marked _dev.
+ */
+#ifndef RAGCACHE_B200_H
+#define RAGCACHE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes; the Python layer maps 1 -> ragsim InsufficientEvictableCapacity
+ * and 2..4 -> ragsim CacheError (tree.py:45-54) */
+#define RCB_OK 0
+#define RCB_ERR_NO_BLOCKS 1
+#define RCB_ERR_BAD_HANDLE 2
+#define RCB_ERR_CUDA 3
+#define RCB_ERR_ARG 4
+
+/* tier selector for rcb_node_blocks (mirrors ragsim Tier, tree.py:39-42) */
+#define RCB_TIER_GPU 0
+#define RCB_TIER_HOST 1
+
+/* swap data paths (rcb_pool_create swap_mode) */
+#define RCB_SWAP_STAGED 0   /* gather kernel -> HBM staging -> cudaMemcpyAsync (and reverse) */
+#define RCB_SWAP_ZEROCOPY 1 /* gather/scatter kernel reading/writing mapped pinned host blocks */
+#define RCB_SWAP_DMA 2      /* cudaMemcpyAsync per contiguous (gpu run, host run) */
+
+const char* rcb_last_error(void);
+int rcb_version(void);
+
+/* ------------------------------------------------------------------ block pool
+ * Paged doc-KV pool: num_gpu_blocks in HBM + num_host_blocks of pinned host
+ * DRAM.  A block holds block_tokens tokens of every layer:
+ *   [n_layers][2 (K,V)][n_kv_heads][block_tokens][head_dim] (elem_bytes each).
+ * Allocation is lowest-free-block-first in both tiers (deterministic, so block
+ * tables are reproducible by the Python oracle, oracle/block_oracle.py).
+ * Node keys are KnowledgeNode.serial (tree.py:94-96); generation keys are
+ * caller-chosen ids of in-flight prefills (simulator.py:84-114). */
+typedef struct rcb_pool rcb_pool;
+
+/* replaces TierState capacity accounting (tree.py:57-67) with real memory.
+ * gpu_base: NULL = the pool cudaMallocs (and zero-fills) its own HBM. */
+int rcb_pool_create(int64_t num_gpu_blocks, int64_t num_host_blocks, int32_t block_tokens,
+                    int32_t n_layers, int32_t n_kv_heads, int32_t head_dim, int32_t elem_bytes,
+                    int32_t swap_mode, void* gpu_base, void* copy_stream, rcb_pool** out);
+int rcb_pool_destroy(rcb_pool* pool);
+/* out[0]=gpu base ptr, out[1]=host base ptr, out[2]=block bytes, out[3]=gpu free blocks,
+ * out[4]=host free blocks, out[5]=num gpu blocks, out[6]=num host blocks */
+int rcb_pool_info(rcb_pool* pool, int64_t* out7);
+/* out[0]=swap-out blocks, out[1]=swap-in blocks, out[2]=D2H bytes, out[3]=H2D bytes,
+ * out[4]=swap-out calls, out[5]=swap-in calls, out[6]=kernel launches, out[7]=memcpy calls */
+int rcb_pool_stats(rcb_pool* pool, int64_t* out8);
+int rcb_pool_set_swap_mode(rcb_pool* pool, int32_t swap_mode);
+
+/* direct node placement (tests / warm start) — new node resident in GPU */
+int rcb_node_alloc_gpu(rcb_pool* pool, int64_t node_key, int32_t n_tokens);
+/* GPU copy dropped with no transfer: swap-out-only-once repeat eviction
+ * (tree.py:456-459) or the node side of _drop_subtree (tree.py:482-502) */
+int rcb_node_free_gpu(rcb_pool* pool, int64_t node_key);
+/* host copy freed: _free_from_host (tree.py:475-480) / dropped descendants */
+int rcb_node_free_host(rcb_pool* pool, int64_t node_key);
+/* first GPU eviction: allocate host blocks, copy D2H, free GPU blocks
+ * (_demote_from_gpu swap branch, tree.py:460-473).  Batched; copies are issued
+ * on the pool's copy stream (call rcb_pool_flush or any swap-in to issue). */
+int rcb_node_swap_out(rcb_pool* pool, const int64_t* node_keys, int32_t n);
+/* promotion of host-resident nodes: allocate GPU blocks, copy H2D, host copy
+ * retained (load_to_gpu, tree.py:296-318) */
+int rcb_node_swap_in(rcb_pool* pool, const int64_t* node_keys, int32_t n);
+/* a generation's transient suffix (reserve_gpu, tree.py:320-327): one segment per
+ * miss document plus one for the prompt, each block-aligned */
+int rcb_gen_reserve(rcb_pool* pool, int64_t gen_key, const int32_t* seg_tokens, int32_t nseg);
+/* a node created by insert_path (tree.py:252-294) takes over the segment that
+ * the generation's prefill already filled — no copy */
+int rcb_node_adopt(rcb_pool* pool, int64_t node_key, int64_t gen_key, int32_t seg_idx);
+/* release_gpu (tree.py:329-333) / _abort (simulator.py:549-559): free every
+ * segment not adopted */
+int rcb_gen_release(rcb_pool* pool, int64_t gen_key);
+
+int rcb_node_blocks(rcb_pool* pool, int64_t node_key, int32_t tier, int32_t* out, int32_t cap,
+                    int32_t* n_out);
+int rcb_gen_blocks(rcb_pool* pool, int64_t gen_key, int32_t seg_idx, int32_t* out, int32_t cap,
+                   int32_t* n_out);
+/* request block table = concat(GPU blocks of node_keys in order) ++ gen segments,
+ * with the valid-token count of every block (node tails) */
+int rcb_block_table(rcb_pool* pool, const int64_t* node_keys, int32_t n_nodes, int64_t gen_key,
+                    int32_t* blocks_out, int32_t* valid_out, int32_t cap, int32_t* n_out);
+
+/* issue batched copies; make `stream` wait for them; make the copy stream wait
+ * for `stream` (block reuse fences); block until copies finish */
+int rcb_pool_flush(rcb_pool* pool);
+int rcb_pool_fence_into(rcb_pool* pool, void* stream);
+int rcb_pool_wait_for(rcb_pool* pool, void* stream);
+int rcb_pool_sync(rcb_pool* pool);
+
+/* ------------------------------------------------------------------ kernels */
+
+/* (1) vectorised block gather/scatter: dst_base[pairs[2i+1]] = src_base[pairs[2i]]
+ * (block_bytes each).  Either base may be device memory or mapped pinned host
+ * memory.  Stand-in replaced: transfer_time (cost_model.py:120-124). */
+int rcb_kv_block_copy(const void* src_base, void* dst_base, int64_t block_bytes,
+                      const int32_t* pairs_dev, int32_t n_pairs, void* stream);
+
+/* RoPE (rotate-half, LLaMA convention) on q and k, then k/v scattered into the
+ * pool at `slots_dev` (slot = block*block_tokens + offset) for `layer`.
+ * q/k/v: bf16 [n_tokens][heads][head_dim] (row strides q_stride/kv_stride in
+ * elements); q_out: bf16 [n_tokens][n_q_heads][head_dim]. */
+int rcb_kv_write_rope(const void* q, int64_t q_stride, const void* k, const void* v,
+                      int64_t kv_stride, void* q_out, const int32_t* positions_dev,
+                      const int32_t* slots_dev, int32_t n_tokens, int32_t n_q_heads,
+                      void* kv_pool, int32_t block_tokens, int32_t n_layers, int32_t n_kv_heads,
+                      int32_t head_dim, int32_t layer, float rope_theta, void* stream);
+
+/* (2) prefix-aware prefill attention (tcgen05/TMEM, TMA-staged K/V pages).
+ * Stand-in replaced: interpolate(profile, alpha, beta) (cost_model.py:106-117,
+ * simulator.py:506).
+ *   q, o        : bf16 [total_q_tokens][n_q_heads][head_dim]
+ *   req_meta_dev: int32 [n_req][5] = {q_start, q_len(beta), q_pos0(alpha), blk_begin, blk_count}
+ *   blk_*_dev   : int32 per block-table entry: pool block id, valid tokens, logical start pos
+ *   work_dev    : int32 [n_work][4] = {req, q_tile, kv_head, n_kv_tiles}
+ *                 (see rcb_attn_plan) */
+int rcb_prefix_prefill(const void* q, void* o, int32_t total_q_tokens, int32_t n_q_heads,
+                       const void* kv_pool, int64_t num_pool_blocks, int32_t block_tokens,
+                       int32_t n_layers, int32_t n_kv_heads, int32_t head_dim, int32_t layer,
+                       const int32_t* req_meta_dev, const int32_t* blk_ids_dev,
+                       const int32_t* blk_valid_dev, const int32_t* blk_pos_dev,
+                       const int32_t* work_dev, int32_t n_work, float softmax_scale,
+                       void* stream);
+/* host-side work planner for rcb_prefix_prefill: writes up to cap items into
+ * work_out (heaviest first) and returns the count in n_work_out.  Inputs are the
+ * host copies of req_meta / blk_valid / blk_pos. */
+int rcb_attn_plan(const int32_t* req_meta, int32_t n_req, const int32_t* blk_valid,
+                  const int32_t* blk_pos, int32_t block_tokens, int32_t n_q_heads,
+                  int32_t n_kv_heads, int32_t* work_out, int32_t cap, int32_t* n_work_out);
+
+/* (3) exact inner-product top-k retrieval, staged (tcgen05 corpus GEMM +
+ * top-k epilogue).  Stand-in replaced: generate_stages / StagedRetrieval
+ * (speculation.py:33-59,149-194) behind the StageProvider seam (simulator.py:228).
+ *   corpus_dev : bf16 [n_rows][dim] (dim % 64 == 0, dim <= 1024)
+ *   queries_dev: bf16 [n_queries][dim], n_queries <= 64
+ *   stage s (0-based) = exact top-k over rows [0, floor((s+1)*n_rows/n_stages))
+ *   ids_out_dev   : int64 [n_queries][n_stages][k] (row + id_offset), score desc / id asc
+ *   scores_out_dev: fp32  [n_queries][n_stages][k]
+ *   workspace: rcb_retrieval_workspace_bytes() bytes of device memory */
+int64_t rcb_retrieval_workspace_bytes(int64_t n_rows, int32_t n_queries, int32_t k,
+                                      int32_t n_stages);
+int rcb_retrieval_topk(const void* corpus_dev, int64_t n_rows, int32_t dim,
+                       const void* queries_dev, int32_t n_queries, int32_t k, int32_t n_stages,
+                       int64_t id_offset, void* workspace_dev, int64_t workspace_bytes,
+                       int64_t* ids_out_dev, float* scores_out_dev, void* stream);
+/* debug / parity: full score matrix fp32 [n_rows][n_queries] from the same GEMM */
+int rcb_retrieval_scores(const void* corpus_dev, int64_t n_rows, int32_t dim,
+                         const void* queries_dev, int32_t n_queries, float* scores_out_dev,
+                         void* stream);
+/* merge per-shard staged top-k lists (after an NCCL allGather), on device:
+ *   in: [n_shards][n_queries][n_stages][k], out: [n_queries][n_stages][k] */
+int rcb_topk_merge_shards(const int64_t* ids_in_dev, const float* scores_in_dev,
+                          int32_t n_shards, int32_t n_queries, int32_t n_stages, int32_t k,
+                          int64_t* ids_out_dev, float* scores_out_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RAGCACHE_B200_H */

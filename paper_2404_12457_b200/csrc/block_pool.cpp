@@ -1,0 +1,535 @@
+// block_pool.cpp — paged doc-KV block pool: HBM tier + pinned host tier.
+//
+// Executes the KV movements that the reference's knowledge tree only counts
+// in tokens (ragsim tree.py:57-67 TierState, :296-333 load/reserve/release,
+// :450-502 demote / free / drop).  Python (the reference's KnowledgeTree,
+// unchanged) makes every decision; this pool owns memory and block ids.
+//
+// Allocation: lowest-free-block-first min-heaps in both tiers, so the block
+// tables are a deterministic function of the tree's event stream
+// (oracle/block_oracle.py restates the same rule).  Nodes are block-aligned
+// (SURVEY H2): a node of n tokens owns ceil(n / block_tokens) blocks.
+//
+// Copies are batched per direction and issued in order on one copy stream
+// (SURVEY H3): a block freed by a pending swap-out can only be rewritten by
+// work that is ordered after the flush (swap-in on the same stream, or compute
+// fenced with rcb_pool_fence_into).
+#include <algorithm>
+#include <cstring>
+#include <functional>
+#include <queue>
+#include <unordered_map>
+#include <vector>
+
+#include "rcb_internal.h"
+
+namespace {
+
+struct MinHeap {
+  std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> q;
+  void init(int64_t n) {
+    std::vector<int32_t> v(n);
+    for (int64_t i = 0; i < n; ++i) v[i] = static_cast<int32_t>(i);
+    q = decltype(q)(std::greater<int32_t>(), std::move(v));
+  }
+  int64_t size() const { return static_cast<int64_t>(q.size()); }
+  void take(int32_t n, std::vector<int32_t>& out) {
+    out.clear();
+    out.reserve(n);
+    for (int32_t i = 0; i < n; ++i) {
+      out.push_back(q.top());
+      q.pop();
+    }
+  }
+  void give(const std::vector<int32_t>& blocks) {
+    for (int32_t b : blocks) q.push(b);
+  }
+};
+
+struct Node {
+  int32_t tokens = 0;
+  std::vector<int32_t> gpu;
+  std::vector<int32_t> host;
+};
+
+struct Seg {
+  int32_t tokens = 0;
+  std::vector<int32_t> blocks;
+  bool adopted = false;
+};
+
+struct Gen {
+  std::vector<Seg> segs;
+};
+
+}  // namespace
+
+struct rcb_pool {
+  int64_t n_gpu = 0, n_host = 0;
+  int32_t bt = 0, layers = 0, kv_heads = 0, head_dim = 0, elem_bytes = 0;
+  int64_t block_bytes = 0;
+  int32_t swap_mode = RCB_SWAP_STAGED;
+  uint8_t* gpu_base = nullptr;
+  bool own_gpu = false;
+  uint8_t* host_base = nullptr;
+  uint8_t* staging = nullptr;
+  int64_t staging_blocks = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaEvent_t ev_done = nullptr, ev_dep = nullptr;
+  MinHeap gpu_free, host_free;
+  std::unordered_map<int64_t, Node> nodes;
+  std::unordered_map<int64_t, Gen> gens;
+  int pending_dir = 0;  // 0 none, 1 gpu->host, 2 host->gpu
+  std::vector<std::pair<int32_t, int32_t>> pending;  // (gpu block, host block)
+  int64_t stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+
+  int32_t nblocks(int32_t tokens) const { return (tokens + bt - 1) / bt; }
+};
+
+namespace {
+
+using rcb::set_cuda_error;
+using rcb::set_error;
+
+int issue_runs(rcb_pool* p, const std::vector<std::pair<int32_t, int32_t>>& pr, size_t lo,
+               size_t hi, bool to_host) {
+  // staged: gather/scatter between pool blocks and staging slots [0, hi-lo), DMA
+  // between staging and host runs.
+  rcb::BlockPairs bp;
+  const int n = static_cast<int>(hi - lo);
+  for (int i = 0; i < n; ++i) {
+    bp.src[i] = to_host ? pr[lo + i].first : i;
+    bp.dst[i] = to_host ? i : pr[lo + i].first;
+  }
+  auto dma_runs = [&](bool d2h) -> int {
+    size_t i = lo;
+    while (i < hi) {
+      size_t j = i + 1;
+      while (j < hi && pr[j].second == pr[j - 1].second + 1) ++j;
+      uint8_t* host = p->host_base + int64_t(pr[i].second) * p->block_bytes;
+      uint8_t* stg = p->staging + int64_t(i - lo) * p->block_bytes;
+      const size_t bytes = size_t(j - i) * p->block_bytes;
+      cudaError_t e = d2h ? cudaMemcpyAsync(host, stg, bytes, cudaMemcpyDeviceToHost, p->stream)
+                          : cudaMemcpyAsync(stg, host, bytes, cudaMemcpyHostToDevice, p->stream);
+      if (e != cudaSuccess) return set_cuda_error(e, "pool staged memcpy");
+      p->stats[7] += 1;
+      i = j;
+    }
+    return RCB_OK;
+  };
+  if (to_host) {
+    cudaError_t e = rcb::launch_block_copy_params(p->gpu_base, p->staging, p->block_bytes, bp, n,
+                                                  p->stream);
+    if (e != cudaSuccess) return set_cuda_error(e, "pool gather");
+    p->stats[6] += 1;
+    return dma_runs(true);
+  }
+  int rc = dma_runs(false);
+  if (rc != RCB_OK) return rc;
+  cudaError_t e =
+      rcb::launch_block_copy_params(p->staging, p->gpu_base, p->block_bytes, bp, n, p->stream);
+  if (e != cudaSuccess) return set_cuda_error(e, "pool scatter");
+  p->stats[6] += 1;
+  return RCB_OK;
+}
+
+int flush(rcb_pool* p) {
+  if (p->pending_dir == 0 || p->pending.empty()) {
+    p->pending_dir = 0;
+    p->pending.clear();
+    return RCB_OK;
+  }
+  const bool to_host = p->pending_dir == 1;
+  auto& pr = p->pending;
+  int rc = RCB_OK;
+  if (p->swap_mode == RCB_SWAP_ZEROCOPY) {
+    for (size_t lo = 0; lo < pr.size() && rc == RCB_OK; lo += rcb::kPairsPerLaunch) {
+      const size_t hi = std::min(pr.size(), lo + rcb::kPairsPerLaunch);
+      rcb::BlockPairs bp;
+      for (size_t i = lo; i < hi; ++i) {
+        bp.src[i - lo] = to_host ? pr[i].first : pr[i].second;
+        bp.dst[i - lo] = to_host ? pr[i].second : pr[i].first;
+      }
+      cudaError_t e = to_host ? rcb::launch_block_copy_params(p->gpu_base, p->host_base,
+                                                              p->block_bytes, bp, int(hi - lo),
+                                                              p->stream)
+                              : rcb::launch_block_copy_params(p->host_base, p->gpu_base,
+                                                              p->block_bytes, bp, int(hi - lo),
+                                                              p->stream);
+      if (e != cudaSuccess) rc = set_cuda_error(e, "pool zero-copy swap");
+      p->stats[6] += 1;
+    }
+  } else if (p->swap_mode == RCB_SWAP_DMA) {
+    size_t i = 0;
+    while (i < pr.size() && rc == RCB_OK) {
+      size_t j = i + 1;
+      while (j < pr.size() && pr[j].first == pr[j - 1].first + 1 &&
+             pr[j].second == pr[j - 1].second + 1)
+        ++j;
+      uint8_t* g = p->gpu_base + int64_t(pr[i].first) * p->block_bytes;
+      uint8_t* h = p->host_base + int64_t(pr[i].second) * p->block_bytes;
+      const size_t bytes = size_t(j - i) * p->block_bytes;
+      cudaError_t e = to_host ? cudaMemcpyAsync(h, g, bytes, cudaMemcpyDeviceToHost, p->stream)
+                              : cudaMemcpyAsync(g, h, bytes, cudaMemcpyHostToDevice, p->stream);
+      if (e != cudaSuccess) rc = set_cuda_error(e, "pool direct memcpy");
+      p->stats[7] += 1;
+      i = j;
+    }
+  } else {
+    const size_t chunk =
+        static_cast<size_t>(std::min<int64_t>(p->staging_blocks, rcb::kPairsPerLaunch));
+    for (size_t lo = 0; lo < pr.size() && rc == RCB_OK; lo += chunk)
+      rc = issue_runs(p, pr, lo, std::min(pr.size(), lo + chunk), to_host);
+  }
+  const int64_t moved = static_cast<int64_t>(pr.size()) * p->block_bytes;
+  if (to_host) p->stats[2] += moved;
+  else p->stats[3] += moved;
+  p->pending.clear();
+  p->pending_dir = 0;
+  return rc;
+}
+
+int enqueue(rcb_pool* p, int dir, const std::vector<int32_t>& g, const std::vector<int32_t>& h) {
+  if (p->pending_dir != 0 && p->pending_dir != dir) {
+    int rc = flush(p);
+    if (rc != RCB_OK) return rc;
+  }
+  p->pending_dir = dir;
+  for (size_t i = 0; i < g.size(); ++i) p->pending.emplace_back(g[i], h[i]);
+  return RCB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rcb_pool_create(int64_t num_gpu_blocks, int64_t num_host_blocks, int32_t block_tokens,
+                    int32_t n_layers, int32_t n_kv_heads, int32_t head_dim, int32_t elem_bytes,
+                    int32_t swap_mode, void* gpu_base, void* copy_stream, rcb_pool** out) {
+  if (out == nullptr) return set_error(RCB_ERR_ARG, "null out");
+  *out = nullptr;
+  if (num_gpu_blocks <= 0 || num_host_blocks < 0 || block_tokens <= 0 || n_layers <= 0 ||
+      n_kv_heads <= 0 || head_dim <= 0 || elem_bytes <= 0 || num_gpu_blocks >= (1ll << 31) ||
+      num_host_blocks >= (1ll << 31))
+    return set_error(RCB_ERR_ARG, "bad pool geometry");
+  if (swap_mode < RCB_SWAP_STAGED || swap_mode > RCB_SWAP_DMA)
+    return set_error(RCB_ERR_ARG, "bad swap mode");
+  rcb_pool* p = new rcb_pool();
+  p->n_gpu = num_gpu_blocks;
+  p->n_host = num_host_blocks;
+  p->bt = block_tokens;
+  p->layers = n_layers;
+  p->kv_heads = n_kv_heads;
+  p->head_dim = head_dim;
+  p->elem_bytes = elem_bytes;
+  p->block_bytes = int64_t(n_layers) * 2 * n_kv_heads * block_tokens * head_dim * elem_bytes;
+  if (p->block_bytes % 16 != 0) {
+    delete p;
+    return set_error(RCB_ERR_ARG, "block bytes must be a multiple of 16");
+  }
+  p->swap_mode = swap_mode;
+  cudaError_t e;
+  if (gpu_base != nullptr) {
+    p->gpu_base = static_cast<uint8_t*>(gpu_base);
+  } else {
+    e = cudaMalloc(&p->gpu_base, num_gpu_blocks * p->block_bytes);
+    if (e != cudaSuccess) {
+      delete p;
+      return set_cuda_error(e, "pool cudaMalloc");
+    }
+    p->own_gpu = true;
+    // attention never reads uninitialised (possibly NaN) bytes from masked slots
+    e = cudaMemset(p->gpu_base, 0, num_gpu_blocks * p->block_bytes);
+    if (e != cudaSuccess) {
+      cudaFree(p->gpu_base);
+      delete p;
+      return set_cuda_error(e, "pool cudaMemset");
+    }
+  }
+  if (num_host_blocks > 0) {
+    e = cudaHostAlloc(&p->host_base, num_host_blocks * p->block_bytes,
+                      cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+      if (p->own_gpu) cudaFree(p->gpu_base);
+      delete p;
+      return set_cuda_error(e, "pool cudaHostAlloc");
+    }
+  }
+  const int64_t staging_cap = std::max<int64_t>(1, (int64_t(256) << 20) / p->block_bytes);
+  p->staging_blocks = std::min<int64_t>(staging_cap, std::max<int64_t>(1, num_host_blocks));
+  e = cudaMalloc(&p->staging, p->staging_blocks * p->block_bytes);
+  if (e == cudaSuccess && copy_stream == nullptr) {
+    e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking);
+    p->own_stream = true;
+  } else {
+    p->stream = static_cast<cudaStream_t>(copy_stream);
+  }
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_dep, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    rcb_pool_destroy(p);
+    return set_cuda_error(e, "pool stream/staging");
+  }
+  p->gpu_free.init(num_gpu_blocks);
+  p->host_free.init(num_host_blocks);
+  *out = p;
+  return RCB_OK;
+}
+
+int rcb_pool_destroy(rcb_pool* p) {
+  if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  if (p->stream) cudaStreamSynchronize(p->stream);
+  if (p->ev_done) cudaEventDestroy(p->ev_done);
+  if (p->ev_dep) cudaEventDestroy(p->ev_dep);
+  if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
+  if (p->staging) cudaFree(p->staging);
+  if (p->host_base) cudaFreeHost(p->host_base);
+  if (p->own_gpu && p->gpu_base) cudaFree(p->gpu_base);
+  delete p;
+  return RCB_OK;
+}
+
+int rcb_pool_info(rcb_pool* p, int64_t* out) {
+  if (p == nullptr || out == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  out[0] = reinterpret_cast<int64_t>(p->gpu_base);
+  out[1] = reinterpret_cast<int64_t>(p->host_base);
+  out[2] = p->block_bytes;
+  out[3] = p->gpu_free.size();
+  out[4] = p->host_free.size();
+  out[5] = p->n_gpu;
+  out[6] = p->n_host;
+  return RCB_OK;
+}
+
+int rcb_pool_stats(rcb_pool* p, int64_t* out) {
+  if (p == nullptr || out == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  std::memcpy(out, p->stats, sizeof(p->stats));
+  return RCB_OK;
+}
+
+int rcb_pool_set_swap_mode(rcb_pool* p, int32_t mode) {
+  if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  if (mode < RCB_SWAP_STAGED || mode > RCB_SWAP_DMA) return set_error(RCB_ERR_ARG, "bad mode");
+  int rc = flush(p);
+  p->swap_mode = mode;
+  return rc;
+}
+
+int rcb_node_alloc_gpu(rcb_pool* p, int64_t key, int32_t n_tokens) {
+  if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  if (n_tokens <= 0) return set_error(RCB_ERR_ARG, "node needs positive tokens");
+  auto it = p->nodes.find(key);
+  if (it != p->nodes.end() && !it->second.gpu.empty())
+    return set_error(RCB_ERR_BAD_HANDLE, "node already GPU-resident");
+  const int32_t nb = p->nblocks(n_tokens);
+  if (p->gpu_free.size() < nb) return set_error(RCB_ERR_NO_BLOCKS, "out of GPU blocks");
+  Node& n = p->nodes[key];
+  n.tokens = n_tokens;
+  p->gpu_free.take(nb, n.gpu);
+  return RCB_OK;
+}
+
+int rcb_node_free_gpu(rcb_pool* p, int64_t key) {
+  if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  auto it = p->nodes.find(key);
+  if (it == p->nodes.end() || it->second.gpu.empty())
+    return set_error(RCB_ERR_BAD_HANDLE, "node not GPU-resident");
+  p->gpu_free.give(it->second.gpu);
+  it->second.gpu.clear();
+  if (it->second.host.empty()) p->nodes.erase(it);
+  return RCB_OK;
+}
+
+int rcb_node_free_host(rcb_pool* p, int64_t key) {
+  if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  auto it = p->nodes.find(key);
+  if (it == p->nodes.end() || it->second.host.empty())
+    return set_error(RCB_ERR_BAD_HANDLE, "node has no host copy");
+  p->host_free.give(it->second.host);
+  it->second.host.clear();
+  if (it->second.gpu.empty()) p->nodes.erase(it);
+  return RCB_OK;
+}
+
+int rcb_node_swap_out(rcb_pool* p, const int64_t* keys, int32_t n) {
+  if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  int64_t need = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    auto it = p->nodes.find(keys[i]);
+    if (it == p->nodes.end() || it->second.gpu.empty() || !it->second.host.empty())
+      return set_error(RCB_ERR_BAD_HANDLE, "swap-out needs a GPU node without host copy");
+    need += p->nblocks(it->second.tokens);
+  }
+  if (p->host_free.size() < need) return set_error(RCB_ERR_NO_BLOCKS, "out of host blocks");
+  for (int32_t i = 0; i < n; ++i) {
+    Node& nd = p->nodes[keys[i]];
+    p->host_free.take(p->nblocks(nd.tokens), nd.host);
+    int rc = enqueue(p, 1, nd.gpu, nd.host);
+    if (rc != RCB_OK) return rc;
+    p->stats[0] += static_cast<int64_t>(nd.gpu.size());
+    p->gpu_free.give(nd.gpu);
+    nd.gpu.clear();
+  }
+  p->stats[4] += 1;
+  return RCB_OK;
+}
+
+int rcb_node_swap_in(rcb_pool* p, const int64_t* keys, int32_t n) {
+  if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  int64_t need = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    auto it = p->nodes.find(keys[i]);
+    if (it == p->nodes.end() || it->second.host.empty() || !it->second.gpu.empty())
+      return set_error(RCB_ERR_BAD_HANDLE, "swap-in needs a host-only node");
+    need += p->nblocks(it->second.tokens);
+  }
+  if (p->gpu_free.size() < need) return set_error(RCB_ERR_NO_BLOCKS, "out of GPU blocks");
+  for (int32_t i = 0; i < n; ++i) {
+    Node& nd = p->nodes[keys[i]];
+    p->gpu_free.take(p->nblocks(nd.tokens), nd.gpu);
+    int rc = enqueue(p, 2, nd.gpu, nd.host);
+    if (rc != RCB_OK) return rc;
+    p->stats[1] += static_cast<int64_t>(nd.gpu.size());
+  }
+  p->stats[5] += 1;
+  return RCB_OK;
+}
+
+int rcb_gen_reserve(rcb_pool* p, int64_t gen_key, const int32_t* seg_tokens, int32_t nseg) {
+  if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  if (p->gens.count(gen_key)) return set_error(RCB_ERR_BAD_HANDLE, "generation already reserved");
+  int64_t need = 0;
+  for (int32_t i = 0; i < nseg; ++i) {
+    if (seg_tokens[i] <= 0) return set_error(RCB_ERR_ARG, "segment needs positive tokens");
+    need += p->nblocks(seg_tokens[i]);
+  }
+  if (p->gpu_free.size() < need) return set_error(RCB_ERR_NO_BLOCKS, "out of GPU blocks");
+  Gen& g = p->gens[gen_key];
+  g.segs.resize(nseg);
+  for (int32_t i = 0; i < nseg; ++i) {
+    g.segs[i].tokens = seg_tokens[i];
+    p->gpu_free.take(p->nblocks(seg_tokens[i]), g.segs[i].blocks);
+  }
+  return RCB_OK;
+}
+
+int rcb_node_adopt(rcb_pool* p, int64_t key, int64_t gen_key, int32_t seg_idx) {
+  if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  auto git = p->gens.find(gen_key);
+  if (git == p->gens.end() || seg_idx < 0 || seg_idx >= (int32_t)git->second.segs.size())
+    return set_error(RCB_ERR_BAD_HANDLE, "unknown generation segment");
+  Seg& s = git->second.segs[seg_idx];
+  if (s.adopted) return set_error(RCB_ERR_BAD_HANDLE, "segment already adopted");
+  auto it = p->nodes.find(key);
+  if (it != p->nodes.end() && !it->second.gpu.empty())
+    return set_error(RCB_ERR_BAD_HANDLE, "adopting node already GPU-resident");
+  Node& nd = p->nodes[key];
+  nd.tokens = s.tokens;
+  nd.gpu = std::move(s.blocks);
+  s.blocks.clear();
+  s.adopted = true;
+  return RCB_OK;
+}
+
+int rcb_gen_release(rcb_pool* p, int64_t gen_key) {
+  if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  auto git = p->gens.find(gen_key);
+  if (git == p->gens.end()) return set_error(RCB_ERR_BAD_HANDLE, "unknown generation");
+  for (Seg& s : git->second.segs)
+    if (!s.adopted) p->gpu_free.give(s.blocks);
+  p->gens.erase(git);
+  return RCB_OK;
+}
+
+static int copy_out(const std::vector<int32_t>& v, int32_t* out, int32_t cap, int32_t* n_out) {
+  if (n_out) *n_out = static_cast<int32_t>(v.size());
+  if (static_cast<int32_t>(v.size()) > cap) return set_error(RCB_ERR_ARG, "output capacity too small");
+  if (out && !v.empty()) std::memcpy(out, v.data(), v.size() * sizeof(int32_t));
+  return RCB_OK;
+}
+
+int rcb_node_blocks(rcb_pool* p, int64_t key, int32_t tier, int32_t* out, int32_t cap,
+                    int32_t* n_out) {
+  if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  auto it = p->nodes.find(key);
+  static const std::vector<int32_t> empty;
+  if (it == p->nodes.end()) return copy_out(empty, out, cap, n_out);
+  return copy_out(tier == RCB_TIER_GPU ? it->second.gpu : it->second.host, out, cap, n_out);
+}
+
+int rcb_gen_blocks(rcb_pool* p, int64_t gen_key, int32_t seg_idx, int32_t* out, int32_t cap,
+                   int32_t* n_out) {
+  if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  auto git = p->gens.find(gen_key);
+  if (git == p->gens.end() || seg_idx < 0 || seg_idx >= (int32_t)git->second.segs.size())
+    return set_error(RCB_ERR_BAD_HANDLE, "unknown generation segment");
+  return copy_out(git->second.segs[seg_idx].blocks, out, cap, n_out);
+}
+
+int rcb_block_table(rcb_pool* p, const int64_t* node_keys, int32_t n_nodes, int64_t gen_key,
+                    int32_t* blocks_out, int32_t* valid_out, int32_t cap, int32_t* n_out) {
+  if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  int32_t n = 0;
+  auto push = [&](const std::vector<int32_t>& blocks, int32_t tokens) -> int {
+    for (size_t i = 0; i < blocks.size(); ++i) {
+      if (n >= cap) return set_error(RCB_ERR_ARG, "block table capacity too small");
+      blocks_out[n] = blocks[i];
+      valid_out[n] = (i + 1 < blocks.size()) ? p->bt : tokens - int32_t(i) * p->bt;
+      ++n;
+    }
+    return RCB_OK;
+  };
+  for (int32_t i = 0; i < n_nodes; ++i) {
+    auto it = p->nodes.find(node_keys[i]);
+    if (it == p->nodes.end() || it->second.gpu.empty())
+      return set_error(RCB_ERR_BAD_HANDLE, "block table node not GPU-resident");
+    int rc = push(it->second.gpu, it->second.tokens);
+    if (rc != RCB_OK) return rc;
+  }
+  if (gen_key >= 0) {
+    auto git = p->gens.find(gen_key);
+    if (git == p->gens.end()) return set_error(RCB_ERR_BAD_HANDLE, "unknown generation");
+    for (const Seg& s : git->second.segs) {
+      if (s.adopted) return set_error(RCB_ERR_BAD_HANDLE, "generation segment already adopted");
+      int rc = push(s.blocks, s.tokens);
+      if (rc != RCB_OK) return rc;
+    }
+  }
+  if (n_out) *n_out = n;
+  return RCB_OK;
+}
+
+int rcb_pool_flush(rcb_pool* p) {
+  if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  return flush(p);
+}
+
+int rcb_pool_fence_into(rcb_pool* p, void* stream) {
+  if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  int rc = flush(p);
+  if (rc != RCB_OK) return rc;
+  cudaError_t e = cudaEventRecord(p->ev_done, p->stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), p->ev_done, 0);
+  if (e != cudaSuccess) return set_cuda_error(e, "pool fence_into");
+  return RCB_OK;
+}
+
+int rcb_pool_wait_for(rcb_pool* p, void* stream) {
+  if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  cudaError_t e = cudaEventRecord(p->ev_dep, static_cast<cudaStream_t>(stream));
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(p->stream, p->ev_dep, 0);
+  if (e != cudaSuccess) return set_cuda_error(e, "pool wait_for");
+  return RCB_OK;
+}
+
+int rcb_pool_sync(rcb_pool* p) {
+  if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  int rc = flush(p);
+  if (rc != RCB_OK) return rc;
+  cudaError_t e = cudaStreamSynchronize(p->stream);
+  if (e != cudaSuccess) return set_cuda_error(e, "pool sync");
+  return RCB_OK;
+}
+
+}  // extern "C"

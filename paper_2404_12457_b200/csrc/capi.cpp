@@ -1,0 +1,136 @@
+// capi.cpp — C-ABI glue: error reporting, TMA descriptor encoding, the
+// prefill entry point and its host-side work planner.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <cudaTypedefs.h>
+#include <string>
+#include <vector>
+
+#include "rcb_internal.h"
+
+namespace rcb {
+
+namespace {
+thread_local std::string g_last_error;
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+}  // namespace
+
+int set_error(int code, const char* msg) {
+  g_last_error = msg ? msg : "";
+  return code;
+}
+
+int set_cuda_error(cudaError_t e, const char* where) {
+  g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return RCB_ERR_CUDA;
+}
+
+int encode_tma_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
+                    const uint64_t* strides, const uint32_t* box) {
+  if (g_encode == nullptr) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || fn == nullptr)
+      return set_error(RCB_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t gdim[5];
+  cuuint64_t gstr[4];
+  cuuint32_t bx[5];
+  cuuint32_t es[5];
+  for (int i = 0; i < rank; ++i) {
+    gdim[i] = dims[i];
+    bx[i] = box[i];
+    es[i] = 1;
+  }
+  for (int i = 0; i + 1 < rank; ++i) gstr[i] = strides[i];
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), gdim,
+                        gstr, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[128];
+    std::snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled failed (CUresult %d, rank %d)",
+                  (int)r, rank);
+    return set_error(RCB_ERR_ARG, buf);
+  }
+  return RCB_OK;
+}
+
+}  // namespace rcb
+
+extern "C" {
+
+const char* rcb_last_error(void) { return rcb::g_last_error.c_str(); }
+
+int rcb_version(void) { return 1; }
+
+int rcb_prefix_prefill(const void* q, void* o, int32_t total_q_tokens, int32_t n_q_heads,
+                       const void* kv_pool, int64_t num_pool_blocks, int32_t block_tokens,
+                       int32_t n_layers, int32_t n_kv_heads, int32_t head_dim, int32_t layer,
+                       const int32_t* req_meta_dev, const int32_t* blk_ids_dev,
+                       const int32_t* blk_valid_dev, const int32_t* blk_pos_dev,
+                       const int32_t* work_dev, int32_t n_work, float softmax_scale,
+                       void* stream) {
+  if (block_tokens != 16 && block_tokens != 32 && block_tokens != 64 && block_tokens != 128)
+    return rcb::set_error(RCB_ERR_ARG, "block_tokens must be 16, 32, 64 or 128");
+  return rcb::prefix_prefill(q, o, total_q_tokens, n_q_heads, kv_pool, num_pool_blocks,
+                             block_tokens, n_layers, n_kv_heads, head_dim, layer, req_meta_dev,
+                             blk_ids_dev, blk_valid_dev, blk_pos_dev, work_dev, n_work,
+                             softmax_scale, static_cast<cudaStream_t>(stream));
+}
+
+// Work items (req, q_tile, kv_head, n_kv_tiles).  A query tile only needs the
+// key tiles up to the slot holding its last query position (causal), so the
+// count is found by a binary search over the table's logical block starts.
+// Items are ordered heaviest-first so long tiles start in the first wave.
+int rcb_attn_plan(const int32_t* req_meta, int32_t n_req, const int32_t* blk_valid,
+                  const int32_t* blk_pos, int32_t block_tokens, int32_t n_q_heads,
+                  int32_t n_kv_heads, int32_t* work_out, int32_t cap, int32_t* n_work_out) {
+  if (n_kv_heads <= 0 || n_q_heads % n_kv_heads != 0 || 128 % (n_q_heads / n_kv_heads) != 0)
+    return rcb::set_error(RCB_ERR_ARG, "unsupported head grouping");
+  const int g = n_q_heads / n_kv_heads;
+  const int tq = 128 / g;
+  struct Item {
+    int32_t r, qt, h, tiles;
+  };
+  std::vector<Item> items;
+  for (int32_t r = 0; r < n_req; ++r) {
+    const int32_t q_len = req_meta[r * 5 + 1];
+    const int32_t q_pos0 = req_meta[r * 5 + 2];
+    const int32_t b0 = req_meta[r * 5 + 3];
+    const int32_t nb = req_meta[r * 5 + 4];
+    if (q_len <= 0) continue;
+    if (nb <= 0) return rcb::set_error(RCB_ERR_ARG, "request with queries but no blocks");
+    const int32_t n_qt = (q_len + tq - 1) / tq;
+    for (int32_t qt = 0; qt < n_qt; ++qt) {
+      const int32_t max_qp = q_pos0 + std::min(q_len, (qt + 1) * tq) - 1;
+      // last block whose start <= max_qp
+      int32_t lo = 0, hi = nb - 1;
+      while (lo < hi) {
+        const int32_t mid = (lo + hi + 1) / 2;
+        if (blk_pos[b0 + mid] <= max_qp) lo = mid;
+        else hi = mid - 1;
+      }
+      const int32_t off = std::min(blk_valid[b0 + lo] - 1, max_qp - blk_pos[b0 + lo]);
+      const int32_t slot = lo * block_tokens + std::max(0, off);
+      const int32_t tiles = slot / 128 + 1;
+      for (int32_t h = 0; h < n_kv_heads; ++h) items.push_back({r, qt, h, tiles});
+    }
+  }
+  std::stable_sort(items.begin(), items.end(),
+                   [](const Item& a, const Item& b) { return a.tiles > b.tiles; });
+  if (n_work_out) *n_work_out = static_cast<int32_t>(items.size());
+  if (static_cast<int32_t>(items.size()) > cap)
+    return rcb::set_error(RCB_ERR_ARG, "work capacity too small");
+  for (size_t i = 0; i < items.size(); ++i) {
+    work_out[4 * i + 0] = items[i].r;
+    work_out[4 * i + 1] = items[i].qt;
+    work_out[4 * i + 2] = items[i].h;
+    work_out[4 * i + 3] = items[i].tiles;
+  }
+  return RCB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,202 @@
+// kv_ops.cu — KV block movement and paged KV writes.
+//
+// (1) block gather/scatter: the data path behind the knowledge tree's tier
+//     transitions (swap-out tree.py:460-473, swap-in tree.py:296-318) which the
+//     reference only prices with transfer_time (cost_model.py:120-124).  One
+//     kernel serves HBM->HBM (staging gather/scatter, compaction) and
+//     HBM<->mapped pinned host (zero-copy swap): 16-byte vector accesses, 8
+//     loads in flight per thread, grid-stride over (pair, 32 KB chunk) units.
+// (2) RoPE + paged KV write: the suffix tokens' K/V (miss docs + prompt) are
+//     rotated and scattered straight into their reserved pool blocks, so a
+//     committed node adopts them with no copy (tree.py:252-294 insert_path).
+#include <cuda_bf16.h>
+
+#include "rcb_internal.h"
+
+namespace rcb {
+
+namespace {
+
+constexpr int kCopyThreads = 256;
+constexpr int kCopyUnroll = 8;
+constexpr int64_t kChunk = int64_t(kCopyThreads) * 16 * kCopyUnroll;  // 32 KB
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void copy_unit(const uint8_t* __restrict__ src,
+                                          uint8_t* __restrict__ dst, int64_t block_bytes,
+                                          int64_t chunk) {
+  const int64_t base = chunk * kChunk + int64_t(threadIdx.x) * 16;
+  uint4 v[kCopyUnroll];
+  if (base + (kCopyUnroll - 1) * kCopyThreads * 16 + 16 <= block_bytes) {
+#pragma unroll
+    for (int u = 0; u < kCopyUnroll; ++u)
+      v[u] = ld_stream(reinterpret_cast<const uint4*>(src + base + u * kCopyThreads * 16));
+#pragma unroll
+    for (int u = 0; u < kCopyUnroll; ++u)
+      *reinterpret_cast<uint4*>(dst + base + u * kCopyThreads * 16) = v[u];
+  } else {
+#pragma unroll
+    for (int u = 0; u < kCopyUnroll; ++u) {
+      const int64_t off = base + u * kCopyThreads * 16;
+      if (off + 16 <= block_bytes) v[u] = ld_stream(reinterpret_cast<const uint4*>(src + off));
+    }
+#pragma unroll
+    for (int u = 0; u < kCopyUnroll; ++u) {
+      const int64_t off = base + u * kCopyThreads * 16;
+      if (off + 16 <= block_bytes) *reinterpret_cast<uint4*>(dst + off) = v[u];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kCopyThreads)
+    block_copy_params_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                             int64_t block_bytes, const __grid_constant__ BlockPairs pairs, int n) {
+  const int64_t cpb = (block_bytes + kChunk - 1) / kChunk;
+  const int64_t units = cpb * n;
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const int i = static_cast<int>(u / cpb);
+    const int64_t c = u - i * cpb;
+    copy_unit(src + int64_t(pairs.src[i]) * block_bytes, dst + int64_t(pairs.dst[i]) * block_bytes,
+              block_bytes, c);
+  }
+}
+
+__global__ void __launch_bounds__(kCopyThreads)
+    block_copy_dev_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                          int64_t block_bytes, const int32_t* __restrict__ pairs, int n) {
+  const int64_t cpb = (block_bytes + kChunk - 1) / kChunk;
+  const int64_t units = cpb * n;
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const int i = static_cast<int>(u / cpb);
+    const int64_t c = u - i * cpb;
+    copy_unit(src + int64_t(pairs[2 * i]) * block_bytes,
+              dst + int64_t(pairs[2 * i + 1]) * block_bytes, block_bytes, c);
+  }
+}
+
+int copy_grid(int64_t block_bytes, int n) {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const int64_t units = ((block_bytes + kChunk - 1) / kChunk) * n;
+  const int64_t cap = int64_t(sms) * 4;
+  return static_cast<int>(units < cap ? units : cap);
+}
+
+// ------------------------------------------------------------------ RoPE + write
+__global__ void __launch_bounds__(256)
+    kv_write_rope_kernel(const __nv_bfloat16* __restrict__ q, int64_t q_stride,
+                         const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
+                         int64_t kv_stride, __nv_bfloat16* __restrict__ q_out,
+                         const int32_t* __restrict__ positions, const int32_t* __restrict__ slots,
+                         int n_q_heads, __nv_bfloat16* __restrict__ pool, int block_tokens,
+                         int64_t block_elems, int n_kv_heads, int head_dim, int layer,
+                         float log2_theta) {
+  const int t = blockIdx.x;
+  const int half = head_dim / 2;
+  const float pos = static_cast<float>(positions[t]);
+  const int slot = slots[t];
+  const int blk = slot / block_tokens;
+  const int off = slot - blk * block_tokens;
+  const int64_t tile = int64_t(block_tokens) * head_dim;
+  __nv_bfloat16* kbase = pool + int64_t(blk) * block_elems +
+                         int64_t(2 * layer) * n_kv_heads * tile + int64_t(off) * head_dim;
+  __nv_bfloat16* vbase = kbase + int64_t(n_kv_heads) * tile;
+  const int rot_items = (n_q_heads + n_kv_heads) * half;
+  const int total = rot_items + n_kv_heads * half;
+  for (int it = threadIdx.x; it < total; it += blockDim.x) {
+    if (it < rot_items) {
+      const int h = it / half;
+      const int i = it - h * half;
+      const float inv_freq = exp2f(-(2.f * i / head_dim) * log2_theta);
+      float sn, cs;
+      sincosf(pos * inv_freq, &sn, &cs);
+      const __nv_bfloat16* src;
+      __nv_bfloat16* dst;
+      if (h < n_q_heads) {
+        src = q + int64_t(t) * q_stride + int64_t(h) * head_dim;
+        dst = q_out + (int64_t(t) * n_q_heads + h) * head_dim;
+      } else {
+        const int kh = h - n_q_heads;
+        src = k + int64_t(t) * kv_stride + int64_t(kh) * head_dim;
+        dst = kbase + int64_t(kh) * tile;
+      }
+      const float x0 = __bfloat162float(src[i]);
+      const float x1 = __bfloat162float(src[i + half]);
+      dst[i] = __float2bfloat16(x0 * cs - x1 * sn);
+      dst[i + half] = __float2bfloat16(x1 * cs + x0 * sn);
+    } else {
+      const int j = it - rot_items;
+      const int h = j / half;
+      const int i = j - h * half;
+      const __nv_bfloat16* src = v + int64_t(t) * kv_stride + int64_t(h) * head_dim;
+      __nv_bfloat16* dst = vbase + int64_t(h) * tile;
+      dst[i] = src[i];
+      dst[i + half] = src[i + half];
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_block_copy_params(const void* src_base, void* dst_base, int64_t block_bytes,
+                                     const BlockPairs& pairs, int n, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  block_copy_params_kernel<<<copy_grid(block_bytes, n), kCopyThreads, 0, stream>>>(
+      static_cast<const uint8_t*>(src_base), static_cast<uint8_t*>(dst_base), block_bytes, pairs,
+      n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_block_copy_dev(const void* src_base, void* dst_base, int64_t block_bytes,
+                                  const int32_t* pairs_dev, int n, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  block_copy_dev_kernel<<<copy_grid(block_bytes, n), kCopyThreads, 0, stream>>>(
+      static_cast<const uint8_t*>(src_base), static_cast<uint8_t*>(dst_base), block_bytes,
+      pairs_dev, n);
+  return cudaGetLastError();
+}
+
+}  // namespace rcb
+
+extern "C" int rcb_kv_block_copy(const void* src_base, void* dst_base, int64_t block_bytes,
+                                 const int32_t* pairs_dev, int32_t n_pairs, void* stream) {
+  if (block_bytes <= 0 || block_bytes % 16 != 0)
+    return rcb::set_error(RCB_ERR_ARG, "block_bytes must be a positive multiple of 16");
+  if (n_pairs < 0) return rcb::set_error(RCB_ERR_ARG, "negative pair count");
+  cudaError_t e = rcb::launch_block_copy_dev(src_base, dst_base, block_bytes, pairs_dev, n_pairs,
+                                             static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return rcb::set_cuda_error(e, "rcb_kv_block_copy");
+  return RCB_OK;
+}
+
+extern "C" int rcb_kv_write_rope(const void* q, int64_t q_stride, const void* k, const void* v,
+                                 int64_t kv_stride, void* q_out, const int32_t* positions_dev,
+                                 const int32_t* slots_dev, int32_t n_tokens, int32_t n_q_heads,
+                                 void* kv_pool, int32_t block_tokens, int32_t n_layers,
+                                 int32_t n_kv_heads, int32_t head_dim, int32_t layer,
+                                 float rope_theta, void* stream) {
+  if (n_tokens == 0) return RCB_OK;
+  if (head_dim % 2 != 0 || layer < 0 || layer >= n_layers)
+    return rcb::set_error(RCB_ERR_ARG, "bad head_dim or layer");
+  const int64_t block_elems = int64_t(n_layers) * 2 * n_kv_heads * block_tokens * head_dim;
+  rcb::kv_write_rope_kernel<<<n_tokens, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(q), q_stride, static_cast<const __nv_bfloat16*>(k),
+      static_cast<const __nv_bfloat16*>(v), kv_stride, static_cast<__nv_bfloat16*>(q_out),
+      positions_dev, slots_dev, n_q_heads, static_cast<__nv_bfloat16*>(kv_pool), block_tokens,
+      block_elems, n_kv_heads, head_dim, layer, log2f(rope_theta));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return rcb::set_cuda_error(e, "rcb_kv_write_rope");
+  return RCB_OK;
+}

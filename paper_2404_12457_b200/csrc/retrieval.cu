@@ -1,0 +1,551 @@
+// retrieval.cu — exact inner-product top-k over the embedding corpus, staged.
+//
+// Replaces the synthetic staged retrieval of the reference
+// (speculation.py:149-194 generate_stages/_perturb, plugged in through the
+// StageProvider seam simulator.py:228,315-324): stage s is the exact top-k
+// over the first (s+1)/S of the scan order, the final stage is the full
+// corpus top-k, and the stages feed the DSP controller (speculation.py:98-146).
+//
+// Corpus GEMM on tcgen05: A = 128 corpus rows x 64-dim atoms (TMA, SW128,
+// 5-stage ring), B = the query batch (<= 64 queries, resident in smem), D in
+// TMEM (double-buffered, 2 x NQ fp32 columns).  Epilogue (4 warps): TMEM ->
+// registers -> transposed smem tile, then each thread owns one
+// (query, row-part) pair and keeps an exact top-8 list in registers
+// (score desc, id asc).  Lists are flushed per stage segment to a workspace;
+// a merge kernel (one warp per segment, warp-shuffle argmax rounds) produces
+// the per-stage prefix top-k.  Bound: HBM (N * dim * 2 bytes per scan).
+#include <cfloat>
+#include <climits>
+
+#include "sm100.cuh"
+#include "rcb_internal.h"
+
+namespace rcb {
+namespace ret {
+
+constexpr int kThreads = 192;
+constexpr int kStages = 5;
+constexpr int kKL = 8;  // list length kept per (query, part); k <= kKL
+constexpr int kMaxSeg = 8;
+constexpr int kMaxAtoms = 16;  // dim <= 1024
+
+struct SegInfo {
+  int n_seg;
+  long long bound[kMaxSeg + 1];   // row boundaries
+  int tile_begin[kMaxSeg + 1];    // first global tile of each segment
+};
+
+__device__ __forceinline__ bool better(float s1, int i1, float s2, int i2) {
+  return s1 > s2 || (s1 == s2 && i1 < i2);
+}
+
+template <int NQ>
+struct Layout {
+  static constexpr int kParts = 128 / NQ;
+  static constexpr uint32_t kAtomQ = NQ * 128;  // bytes of one 64-dim atom of the query block
+  static constexpr uint32_t kA = 16384;         // one A stage (128 rows x 128 B)
+  static constexpr int kTStride = 129;          // transposed tile row stride (floats)
+  static uint32_t total(int atoms) {
+    return atoms * kAtomQ + kStages * kA + NQ * kTStride * 4 + 256 + 1024;
+  }
+};
+
+template <int NQ>
+__device__ __forceinline__ void tmem_ld_row(uint32_t taddr, float (&v)[NQ]) {
+#pragma unroll
+  for (int c = 0; c < NQ / 16; ++c) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr + c * 16));
+    tmem_wait_ld();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[c * 16 + i] = __uint_as_float(r[i]);
+  }
+}
+
+template <int NQ>
+__global__ void __launch_bounds__(kThreads, 1)
+    topk_scan_kernel(const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_q,
+                     int atoms, int n_tiles, const __grid_constant__ SegInfo seg,
+                     float* __restrict__ part_score, int* __restrict__ part_id,
+                     float* __restrict__ scores_out, int n_queries) {
+  using Lay = Layout<NQ>;
+  constexpr int kParts = Lay::kParts;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sA = sQ + atoms * Lay::kAtomQ;
+  float* sT = reinterpret_cast<float*>(sA + kStages * Lay::kA);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sT) + NQ * Lay::kTStride * 4);
+  uint64_t* full = bar;                 // [kStages]
+  uint64_t* empty = bar + kStages;      // [kStages]
+  uint64_t* acc_full = bar + 2 * kStages;   // [2]
+  uint64_t* acc_empty = acc_full + 2;       // [2]
+  uint64_t* q_full = acc_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 1);
+
+  const int warp = threadIdx.x >> 5;
+  constexpr uint32_t kTmemCols = (2 * NQ <= 32) ? 32 : (2 * NQ <= 64 ? 64 : 128);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 128);
+    }
+    mbar_init(q_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  auto tile_rows = [&](int t, int& sg, long long& r0, long long& r1) {
+    sg = 0;
+    while (sg + 1 < seg.n_seg && t >= seg.tile_begin[sg + 1]) ++sg;
+    r0 = seg.bound[sg] + (long long)(t - seg.tile_begin[sg]) * 128;
+    r1 = r0 + 128;
+    if (r1 > seg.bound[sg + 1]) r1 = seg.bound[sg + 1];
+  };
+
+  if (warp == 4) {
+    if (elect_one()) {
+      tma_prefetch(&tm_c);
+      tma_prefetch(&tm_q);
+      mbar_arrive_expect_tx(q_full, atoms * Lay::kAtomQ);
+      for (int a = 0; a < atoms; ++a) tma_load_2d(sQ + a * Lay::kAtomQ, &tm_q, q_full, a * 64, 0);
+      int it = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        int sg;
+        long long r0, r1;
+        tile_rows(t, sg, r0, r1);
+        for (int a = 0; a < atoms; ++a, ++it) {
+          const int st = it % kStages;
+          mbar_wait(&empty[st], ((it / kStages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[st], Lay::kA);
+          tma_load_2d(sA + st * Lay::kA, &tm_c, &full[st], a * 64, (int)r0);
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (elect_one()) {
+      constexpr uint32_t idesc = idesc_bf16_f32(128, NQ, 0, 0);
+      const uint32_t a_base = smem_u32(sA);
+      const uint32_t q_base = smem_u32(sQ);
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      int it = 0, li = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++li) {
+        const int buf = li & 1;
+        mbar_wait(&acc_empty[buf], ((li >> 1) & 1) ^ 1);
+        tc_fence_after();
+        for (int a = 0; a < atoms; ++a, ++it) {
+          const int st = it % kStages;
+          mbar_wait(&full[st], (it / kStages) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t da = sw128_desc(a_base + st * Lay::kA + kk * 32, 16, 1024);
+            const uint64_t db = sw128_desc(q_base + a * Lay::kAtomQ + kk * 32, 16, 1024);
+            umma_bf16_ss(tmem + buf * NQ, da, db, idesc, (a > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[st]);
+        }
+        umma_commit(&acc_full[buf]);
+      }
+    }
+  } else {
+    // epilogue: 128 threads
+    const int tid = threadIdx.x;
+    const int q = tid % NQ;
+    const int part = tid / NQ;
+    const uint32_t t_row = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    float ls[kKL];
+    int li_[kKL];
+#pragma unroll
+    for (int i = 0; i < kKL; ++i) { ls[i] = -INFINITY; li_[i] = INT_MAX; }
+    int cur_seg = -1;
+    unsigned flushed = 0;
+    const int P_total = gridDim.x * kParts;
+    auto flush = [&](int sg) {
+      const long long base =
+          (((long long)sg * P_total + (long long)blockIdx.x * kParts + part) * NQ + q) * kKL;
+#pragma unroll
+      for (int i = 0; i < kKL; ++i) {
+        part_score[base + i] = ls[i];
+        part_id[base + i] = li_[i];
+        ls[i] = -INFINITY;
+        li_[i] = INT_MAX;
+      }
+      flushed |= 1u << sg;
+    };
+    int li = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++li) {
+      int sg;
+      long long r0, r1;
+      tile_rows(t, sg, r0, r1);
+      if (sg != cur_seg) {
+        if (cur_seg >= 0) flush(cur_seg);
+        cur_seg = sg;
+      }
+      const int buf = li & 1;
+      mbar_wait(&acc_full[buf], (li >> 1) & 1);
+      tc_fence_after();
+      float v[NQ];
+      tmem_ld_row<NQ>(t_row + buf * NQ, v);
+      tc_fence_before();
+      mbar_arrive(&acc_empty[buf]);
+      if (scores_out != nullptr && r0 + tid < r1) {
+#pragma unroll
+        for (int c = 0; c < NQ; ++c)
+          if (c < n_queries) scores_out[(r0 + tid) * n_queries + c] = v[c];
+      }
+#pragma unroll
+      for (int c = 0; c < NQ; ++c) sT[c * Lay::kTStride + tid] = v[c];
+      named_bar_sync(1, 128);
+      const int row_lo = part * NQ;
+      const long long nvalid = r1 - r0;
+      for (int r = 0; r < NQ; ++r) {
+        const int rr = row_lo + r;
+        if (rr >= nvalid) break;
+        const float sc = sT[q * Lay::kTStride + rr];
+        const int id = (int)(r0 + rr);
+        if (better(sc, id, ls[kKL - 1], li_[kKL - 1])) {
+          // branchless sorted insert
+          bool prev = true;  // "e is better than entry i-1" for i = 0
+#pragma unroll
+          for (int i = kKL - 1; i >= 0; --i) {
+            const bool bi = better(sc, id, ls[i], li_[i]);
+            const bool bprev = (i == 0) ? false : better(sc, id, ls[i - 1], li_[i - 1]);
+            if (bi) {
+              ls[i] = bprev ? ls[i - 1] : sc;
+              li_[i] = bprev ? li_[i - 1] : id;
+            }
+          }
+          (void)prev;
+        }
+      }
+      named_bar_sync(1, 128);
+    }
+    if (cur_seg >= 0) flush(cur_seg);
+    for (int sg = 0; sg < seg.n_seg; ++sg)
+      if (!(flushed & (1u << sg))) flush(sg);
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem);
+  }
+}
+
+// warp-level exact top-k over candidates held as a sorted local list per lane
+__device__ __forceinline__ void warp_topk_emit(float (&ls)[kKL], int (&li)[kKL], int k,
+                                               float* out_s, int* out_i) {
+  int head = 0;
+  for (int r = 0; r < k; ++r) {
+    float s = head < kKL ? ls[0] : -INFINITY;
+    int id = head < kKL ? li[0] : INT_MAX;
+    // the head is always ls[0]; entries shift down after a win
+    float bs = s;
+    int bi = id;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float os = __shfl_xor_sync(0xffffffffu, bs, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (better(os, oi, bs, bi)) { bs = os; bi = oi; }
+    }
+    if (lane_id() == 0) { out_s[r] = bs; out_i[r] = bi; }
+    if (bi == id && bs == s && bi != INT_MAX) {
+#pragma unroll
+      for (int i = 0; i < kKL - 1; ++i) { ls[i] = ls[i + 1]; li[i] = li[i + 1]; }
+      ls[kKL - 1] = -INFINITY;
+      li[kKL - 1] = INT_MAX;
+      ++head;
+    }
+  }
+}
+
+__device__ __forceinline__ void list_insert(float (&ls)[kKL], int (&li)[kKL], float sc, int id) {
+  if (!better(sc, id, ls[kKL - 1], li[kKL - 1])) return;
+#pragma unroll
+  for (int i = kKL - 1; i >= 0; --i) {
+    const bool bi = better(sc, id, ls[i], li[i]);
+    const bool bprev = (i == 0) ? false : better(sc, id, ls[i - 1], li[i - 1]);
+    if (bi) {
+      ls[i] = bprev ? ls[i - 1] : sc;
+      li[i] = bprev ? li[i - 1] : id;
+    }
+  }
+}
+
+// grid = n_queries, block = 32 * n_seg; warp s reduces segment s, then emits stage s
+__global__ void topk_merge_kernel(const float* __restrict__ part_score,
+                                  const int* __restrict__ part_id, int P_total, int NQ, int n_seg,
+                                  int k, long long id_offset, long long* __restrict__ ids_out,
+                                  float* __restrict__ scores_out) {
+  __shared__ float seg_s[kMaxSeg][kKL];
+  __shared__ int seg_i[kMaxSeg][kKL];
+  const int q = blockIdx.x;
+  const int s = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  float ls[kKL];
+  int li[kKL];
+#pragma unroll
+  for (int i = 0; i < kKL; ++i) { ls[i] = -INFINITY; li[i] = INT_MAX; }
+  const long long n_cand = (long long)P_total * kKL;
+  for (long long c = lane; c < n_cand; c += 32) {
+    const long long p = c / kKL, e = c % kKL;
+    const long long idx = (((long long)s * P_total + p) * NQ + q) * kKL + e;
+    list_insert(ls, li, part_score[idx], part_id[idx]);
+  }
+  warp_topk_emit(ls, li, kKL, seg_s[s], seg_i[s]);
+  __syncthreads();
+  // stage s = prefix merge of segments 0..s
+#pragma unroll
+  for (int i = 0; i < kKL; ++i) { ls[i] = -INFINITY; li[i] = INT_MAX; }
+  for (int c = lane; c < (s + 1) * kKL; c += 32) list_insert(ls, li, seg_s[c / kKL][c % kKL], seg_i[c / kKL][c % kKL]);
+  __shared__ float out_s[kMaxSeg][kKL];
+  __shared__ int out_i[kMaxSeg][kKL];
+  warp_topk_emit(ls, li, k, out_s[s], out_i[s]);
+  __syncwarp();
+  if (lane < k) {
+    const long long o = ((long long)q * n_seg + s) * k + lane;
+    const int id = out_i[s][lane];
+    ids_out[o] = (id == INT_MAX) ? -1 : (long long)id + id_offset;
+    scores_out[o] = out_s[s][lane];
+  }
+}
+
+// grid = n_queries * n_stages, block = 32
+__global__ void shard_merge_kernel(const long long* __restrict__ ids_in,
+                                   const float* __restrict__ scores_in, int n_shards, int nq,
+                                   int n_stages, int k, long long* __restrict__ ids_out,
+                                   float* __restrict__ scores_out) {
+  const int qs = blockIdx.x;  // q * n_stages + s
+  const int lane = threadIdx.x;
+  // candidates carry int64 ids; rank them with (score desc, id asc)
+  float bs_list[kKL];
+  long long bi_list[kKL];
+#pragma unroll
+  for (int i = 0; i < kKL; ++i) { bs_list[i] = -INFINITY; bi_list[i] = LLONG_MAX; }
+  for (int c = lane; c < n_shards * k; c += 32) {
+    const int sh = c / k, e = c % k;
+    const long long idx = ((long long)sh * nq * n_stages + qs) * k + e;
+    const float sc = scores_in[idx];
+    long long id = ids_in[idx];
+    if (id < 0) id = LLONG_MAX;
+    if (sc > bs_list[kKL - 1] || (sc == bs_list[kKL - 1] && id < bi_list[kKL - 1])) {
+#pragma unroll
+      for (int i = kKL - 1; i >= 0; --i) {
+        const bool bi = sc > bs_list[i] || (sc == bs_list[i] && id < bi_list[i]);
+        const bool bp = (i == 0) ? false
+                                 : (sc > bs_list[i - 1] || (sc == bs_list[i - 1] && id < bi_list[i - 1]));
+        if (bi) {
+          bs_list[i] = bp ? bs_list[i - 1] : sc;
+          bi_list[i] = bp ? bi_list[i - 1] : id;
+        }
+      }
+    }
+  }
+  for (int r = 0; r < k; ++r) {
+    float bs = bs_list[0];
+    long long bi = bi_list[0];
+    const float mys = bs;
+    const long long myi = bi;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float os = __shfl_xor_sync(0xffffffffu, bs, o);
+      const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (os > bs || (os == bs && oi < bi)) { bs = os; bi = oi; }
+    }
+    if (lane == 0) {
+      ids_out[(long long)qs * k + r] = (bi == LLONG_MAX) ? -1 : bi;
+      scores_out[(long long)qs * k + r] = bs;
+    }
+    if (bi == myi && bs == mys && bi != LLONG_MAX) {
+#pragma unroll
+      for (int i = 0; i < kKL - 1; ++i) { bs_list[i] = bs_list[i + 1]; bi_list[i] = bi_list[i + 1]; }
+      bs_list[kKL - 1] = -INFINITY;
+      bi_list[kKL - 1] = LLONG_MAX;
+    }
+  }
+}
+
+int num_sms() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+int nq_pad(int n) { return n <= 16 ? 16 : (n <= 32 ? 32 : 64); }
+
+void make_segments(int64_t n_rows, int n_stages, SegInfo& seg, int& n_tiles) {
+  seg.n_seg = n_stages;
+  int t = 0;
+  for (int s = 0; s <= n_stages; ++s) seg.bound[s] = (long long)((n_rows * s) / n_stages);
+  for (int s = 0; s < n_stages; ++s) {
+    seg.tile_begin[s] = t;
+    const long long len = seg.bound[s + 1] - seg.bound[s];
+    t += (int)((len + 127) / 128);
+  }
+  seg.tile_begin[n_stages] = t;
+  for (int s = n_stages + 1; s <= kMaxSeg; ++s) { seg.bound[s] = n_rows; seg.tile_begin[s] = t; }
+  n_tiles = t;
+}
+
+int grid_for(int n_tiles) {
+  const int g = num_sms();
+  return n_tiles < g ? (n_tiles > 0 ? n_tiles : 1) : g;
+}
+
+template <int NQ>
+int run_scan(const void* corpus, int64_t n_rows, int dim, const void* queries, int n_queries,
+             int n_stages, float* part_score, int* part_id, float* scores_out, int grid,
+             cudaStream_t stream) {
+  SegInfo seg;
+  int n_tiles;
+  make_segments(n_rows, n_stages, seg, n_tiles);
+  CUtensorMap tc, tq;
+  {
+    const uint64_t dims[2] = {(uint64_t)dim, (uint64_t)n_rows};
+    const uint64_t strides[1] = {(uint64_t)dim * 2};
+    const uint32_t box[2] = {64, 128};
+    int rc = encode_tma_bf16(&tc, corpus, 2, dims, strides, box);
+    if (rc != RCB_OK) return rc;
+  }
+  {
+    const uint64_t dims[2] = {(uint64_t)dim, (uint64_t)n_queries};
+    const uint64_t strides[1] = {(uint64_t)dim * 2};
+    const uint32_t box[2] = {64, (uint32_t)NQ};
+    int rc = encode_tma_bf16(&tq, queries, 2, dims, strides, box);
+    if (rc != RCB_OK) return rc;
+  }
+  const int atoms = dim / 64;
+  const uint32_t smem = Layout<NQ>::total(atoms);
+  auto kern = topk_scan_kernel<NQ>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return set_cuda_error(e, "retrieval smem attr");
+  kern<<<grid, kThreads, smem, stream>>>(tc, tq, atoms, n_tiles, seg, part_score, part_id,
+                                         scores_out, n_queries);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "retrieval scan launch");
+  return RCB_OK;
+}
+
+int scan(const void* corpus, int64_t n_rows, int dim, const void* queries, int n_queries,
+         int n_stages, float* part_score, int* part_id, float* scores_out, int grid,
+         cudaStream_t stream) {
+  switch (nq_pad(n_queries)) {
+    case 16: return run_scan<16>(corpus, n_rows, dim, queries, n_queries, n_stages, part_score, part_id, scores_out, grid, stream);
+    case 32: return run_scan<32>(corpus, n_rows, dim, queries, n_queries, n_stages, part_score, part_id, scores_out, grid, stream);
+    default: return run_scan<64>(corpus, n_rows, dim, queries, n_queries, n_stages, part_score, part_id, scores_out, grid, stream);
+  }
+}
+
+int check_args(int64_t n_rows, int dim, int n_queries, int n_stages) {
+  if (n_rows <= 0 || n_rows >= INT_MAX) return set_error(RCB_ERR_ARG, "n_rows out of range");
+  if (dim <= 0 || dim % 64 != 0 || dim / 64 > kMaxAtoms) return set_error(RCB_ERR_ARG, "dim must be a multiple of 64, <= 1024");
+  if (n_queries <= 0 || n_queries > 64) return set_error(RCB_ERR_ARG, "1 <= n_queries <= 64");
+  if (n_stages <= 0 || n_stages > kMaxSeg) return set_error(RCB_ERR_ARG, "1 <= n_stages <= 8");
+  return RCB_OK;
+}
+
+}  // namespace ret
+}  // namespace rcb
+
+using namespace rcb;
+
+extern "C" int64_t rcb_retrieval_workspace_bytes(int64_t n_rows, int32_t n_queries, int32_t k,
+                                                 int32_t n_stages) {
+  (void)k;
+  ret::SegInfo seg;
+  int n_tiles;
+  ret::make_segments(n_rows, n_stages, seg, n_tiles);
+  const int grid = ret::grid_for(n_tiles);
+  const int nq = ret::nq_pad(n_queries);
+  const int64_t P_total = int64_t(grid) * (128 / nq);
+  return int64_t(n_stages) * P_total * nq * ret::kKL * 8;
+}
+
+extern "C" int rcb_retrieval_topk(const void* corpus_dev, int64_t n_rows, int32_t dim,
+                                  const void* queries_dev, int32_t n_queries, int32_t k,
+                                  int32_t n_stages, int64_t id_offset, void* workspace_dev,
+                                  int64_t workspace_bytes, int64_t* ids_out_dev,
+                                  float* scores_out_dev, void* stream) {
+  int rc = ret::check_args(n_rows, dim, n_queries, n_stages);
+  if (rc != RCB_OK) return rc;
+  if (k < 1 || k > ret::kKL) return set_error(RCB_ERR_ARG, "1 <= k <= 8");
+  const int64_t need = rcb_retrieval_workspace_bytes(n_rows, n_queries, k, n_stages);
+  if (workspace_bytes < need) return set_error(RCB_ERR_ARG, "retrieval workspace too small");
+  ret::SegInfo seg;
+  int n_tiles;
+  ret::make_segments(n_rows, n_stages, seg, n_tiles);
+  const int grid = ret::grid_for(n_tiles);
+  const int nq = ret::nq_pad(n_queries);
+  const int64_t P_total = int64_t(grid) * (128 / nq);
+  float* ps = static_cast<float*>(workspace_dev);
+  int* pi = reinterpret_cast<int*>(ps + int64_t(n_stages) * P_total * nq * ret::kKL);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  rc = ret::scan(corpus_dev, n_rows, dim, queries_dev, n_queries, n_stages, ps, pi, nullptr, grid, st);
+  if (rc != RCB_OK) return rc;
+  ret::topk_merge_kernel<<<n_queries, 32 * n_stages, 0, st>>>(
+      ps, pi, (int)P_total, nq, n_stages, k, id_offset, reinterpret_cast<long long*>(ids_out_dev),
+      scores_out_dev);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "retrieval merge launch");
+  return RCB_OK;
+}
+
+extern "C" int rcb_retrieval_scores(const void* corpus_dev, int64_t n_rows, int32_t dim,
+                                    const void* queries_dev, int32_t n_queries,
+                                    float* scores_out_dev, void* stream) {
+  int rc = ret::check_args(n_rows, dim, n_queries, 1);
+  if (rc != RCB_OK) return rc;
+  ret::SegInfo seg;
+  int n_tiles;
+  ret::make_segments(n_rows, 1, seg, n_tiles);
+  const int grid = ret::grid_for(n_tiles);
+  const int nq = ret::nq_pad(n_queries);
+  const int64_t P_total = int64_t(grid) * (128 / nq);
+  const int64_t ws = P_total * nq * ret::kKL * 8;
+  void* buf = nullptr;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMallocAsync(&buf, ws, st);
+  if (e != cudaSuccess) return set_cuda_error(e, "retrieval scores workspace");
+  float* ps = static_cast<float*>(buf);
+  int* pi = reinterpret_cast<int*>(ps + P_total * nq * ret::kKL);
+  rc = ret::scan(corpus_dev, n_rows, dim, queries_dev, n_queries, 1, ps, pi, scores_out_dev, grid, st);
+  cudaFreeAsync(buf, st);
+  return rc;
+}
+
+extern "C" int rcb_topk_merge_shards(const int64_t* ids_in_dev, const float* scores_in_dev,
+                                     int32_t n_shards, int32_t n_queries, int32_t n_stages,
+                                     int32_t k, int64_t* ids_out_dev, float* scores_out_dev,
+                                     void* stream) {
+  if (n_shards < 1 || n_queries < 1 || n_stages < 1 || k < 1 || k > ret::kKL)
+    return set_error(RCB_ERR_ARG, "bad shard-merge shape");
+  ret::shard_merge_kernel<<<n_queries * n_stages, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const long long*>(ids_in_dev), scores_in_dev, n_shards, n_queries,
+      n_stages, k, reinterpret_cast<long long*>(ids_out_dev), scores_out_dev);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "shard merge launch");
+  return RCB_OK;
+}

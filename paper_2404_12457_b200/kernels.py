@@ -1,0 +1,174 @@
+"""Thin torch-facing wrappers over the C-ABI kernels.
+
+torch is used only as device-memory/stream plumbing: every call passes raw
+pointers to libragcache_b200.so (include/ragcache_b200.h).  No CPU path: a
+missing library raises RcbUnavailable, a non-CUDA tensor raises ValueError.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, load
+
+
+def _dev_ptr(t: torch.Tensor) -> int:
+    if not t.is_cuda:
+        raise ValueError("rcb kernels take CUDA tensors only (no CPU fallback)")
+    return t.data_ptr()
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return _lib.stream_handle(stream)
+
+
+def block_copy(src_base: int, dst_base: int, block_bytes: int, pairs: torch.Tensor,
+               stream=None) -> None:
+    """dst[pairs[i,1]] = src[pairs[i,0]] for block_bytes-sized blocks (device/mapped ptrs)."""
+    pairs = pairs.to(dtype=torch.int32).contiguous()
+    check(load().rcb_kv_block_copy(src_base, dst_base, block_bytes, _dev_ptr(pairs),
+                                   pairs.shape[0], _stream(stream)), "rcb_kv_block_copy")
+
+
+def kv_write_rope(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, q_out: torch.Tensor,
+                  positions: torch.Tensor, slots: torch.Tensor, pool_base: int, *,
+                  block_tokens: int, n_layers: int, n_kv_heads: int, head_dim: int,
+                  layer: int, rope_theta: float, stream=None) -> None:
+    """RoPE q,k then scatter k,v into the pool (q/k/v may be strided row views)."""
+    n_tokens = q.shape[0]
+    n_q_heads = q_out.shape[1]
+    assert q.stride(-1) == 1 and k.stride(-1) == 1 and v.stride(-1) == 1
+    assert k.stride(0) == v.stride(0)
+    check(load().rcb_kv_write_rope(
+        _dev_ptr(q), q.stride(0), _dev_ptr(k), _dev_ptr(v), k.stride(0), _dev_ptr(q_out),
+        _dev_ptr(positions), _dev_ptr(slots), n_tokens, n_q_heads, pool_base, block_tokens,
+        n_layers, n_kv_heads, head_dim, layer, float(rope_theta), _stream(stream)),
+        "rcb_kv_write_rope")
+
+
+class AttnPlan:
+    """Device-resident block tables + work list for one prefill batch.
+
+    requests: list of (q_len, q_pos0, blocks, valid) — blocks/valid are the
+    request's block table (cached prefix nodes then suffix segments) as
+    produced by BlockPool.block_table.
+    """
+
+    def __init__(self, requests, *, block_tokens: int, n_q_heads: int, n_kv_heads: int,
+                 device="cuda") -> None:
+        meta = []
+        ids: list[int] = []
+        valid: list[int] = []
+        pos: list[int] = []
+        q_start = 0
+        for q_len, q_pos0, blocks, vals in requests:
+            meta.extend([q_start, q_len, q_pos0, len(ids), len(blocks)])
+            acc = 0
+            for b, v in zip(blocks, vals):
+                ids.append(int(b))
+                valid.append(int(v))
+                pos.append(acc)
+                acc += int(v)
+            if acc != q_pos0 + q_len:
+                raise ValueError(f"block table covers {acc} tokens, expected {q_pos0 + q_len}")
+            q_start += q_len
+        self.total_q = q_start
+        self.n_req = len(requests)
+        meta_np = np.asarray(meta, dtype=np.int32)
+        valid_np = np.asarray(valid, dtype=np.int32)
+        pos_np = np.asarray(pos, dtype=np.int32)
+        g = n_q_heads // n_kv_heads
+        cap = sum(max(0, -(-r[0] // (128 // g))) for r in requests) * n_kv_heads + 1
+        work = np.zeros(cap * 4, dtype=np.int32)
+        n_work = np.zeros(1, dtype=np.int32)
+        check(load().rcb_attn_plan(
+            meta_np.ctypes.data_as(_lib._p32), self.n_req, valid_np.ctypes.data_as(_lib._p32),
+            pos_np.ctypes.data_as(_lib._p32), block_tokens, n_q_heads, n_kv_heads,
+            work.ctypes.data_as(_lib._p32), cap, n_work.ctypes.data_as(_lib._p32)),
+            "rcb_attn_plan")
+        self.n_work = int(n_work[0])
+        self.work_host = work[: self.n_work * 4].reshape(-1, 4)
+        self.kv_tiles = int(self.work_host[:, 3].sum()) if self.n_work else 0
+        pack = np.concatenate([meta_np, np.asarray(ids, dtype=np.int32), valid_np, pos_np,
+                               work[: self.n_work * 4]])
+        self._buf = torch.from_numpy(pack).to(device)
+        o = 0
+        self.meta = self._buf[o:o + meta_np.size]; o += meta_np.size
+        self.blk_ids = self._buf[o:o + len(ids)]; o += len(ids)
+        self.blk_valid = self._buf[o:o + len(ids)]; o += len(ids)
+        self.blk_pos = self._buf[o:o + len(ids)]; o += len(ids)
+        self.work = self._buf[o:o + self.n_work * 4]
+        self.requests = requests
+
+
+def prefix_prefill(q: torch.Tensor, out: torch.Tensor, plan: AttnPlan, pool_base: int,
+                   num_pool_blocks: int, *, block_tokens: int, n_layers: int, n_kv_heads: int,
+                   head_dim: int, layer: int, softmax_scale: float | None = None,
+                   stream=None) -> None:
+    """Prefix-aware prefill attention for one layer (tcgen05 kernel)."""
+    assert q.dtype == torch.bfloat16 and q.is_contiguous() and out.is_contiguous()
+    n_q_heads = q.shape[1]
+    if softmax_scale is None:
+        softmax_scale = 1.0 / math.sqrt(head_dim)
+    check(load().rcb_prefix_prefill(
+        _dev_ptr(q), _dev_ptr(out), q.shape[0], n_q_heads, pool_base, num_pool_blocks,
+        block_tokens, n_layers, n_kv_heads, head_dim, layer, _dev_ptr(plan.meta),
+        _dev_ptr(plan.blk_ids), _dev_ptr(plan.blk_valid), _dev_ptr(plan.blk_pos),
+        _dev_ptr(plan.work), plan.n_work, float(softmax_scale), _stream(stream)),
+        "rcb_prefix_prefill")
+
+
+class RetrievalWorkspace:
+    def __init__(self, n_rows: int, n_queries: int, k: int, n_stages: int, device="cuda"):
+        self.nbytes = int(load().rcb_retrieval_workspace_bytes(n_rows, n_queries, k, n_stages))
+        self.buf = torch.empty(max(16, self.nbytes), dtype=torch.uint8, device=device)
+        self.key = (n_rows, n_queries, k, n_stages)
+
+
+def retrieval_topk(corpus: torch.Tensor, queries: torch.Tensor, k: int, n_stages: int,
+                   id_offset: int = 0, workspace: RetrievalWorkspace | None = None,
+                   ids_out: torch.Tensor | None = None, scores_out: torch.Tensor | None = None,
+                   stream=None):
+    """Staged exact top-k: returns (ids int64 [b,S,k], scores fp32 [b,S,k])."""
+    assert corpus.dtype == torch.bfloat16 and queries.dtype == torch.bfloat16
+    n_rows, dim = corpus.shape
+    b = queries.shape[0]
+    if workspace is None or workspace.key != (n_rows, b, k, n_stages):
+        workspace = RetrievalWorkspace(n_rows, b, k, n_stages, corpus.device)
+    if ids_out is None:
+        ids_out = torch.empty((b, n_stages, k), dtype=torch.int64, device=corpus.device)
+    if scores_out is None:
+        scores_out = torch.empty((b, n_stages, k), dtype=torch.float32, device=corpus.device)
+    check(load().rcb_retrieval_topk(
+        _dev_ptr(corpus), n_rows, dim, _dev_ptr(queries), b, k, n_stages, id_offset,
+        _dev_ptr(workspace.buf), workspace.nbytes, _dev_ptr(ids_out), _dev_ptr(scores_out),
+        _stream(stream)), "rcb_retrieval_topk")
+    return ids_out, scores_out
+
+
+def retrieval_scores(corpus: torch.Tensor, queries: torch.Tensor, stream=None) -> torch.Tensor:
+    n_rows, dim = corpus.shape
+    b = queries.shape[0]
+    out = torch.empty((n_rows, b), dtype=torch.float32, device=corpus.device)
+    check(load().rcb_retrieval_scores(_dev_ptr(corpus), n_rows, dim, _dev_ptr(queries), b,
+                                      _dev_ptr(out), _stream(stream)), "rcb_retrieval_scores")
+    return out
+
+
+def topk_merge_shards(ids: torch.Tensor, scores: torch.Tensor, stream=None):
+    """ids/scores [n_shards, b, S, k] -> merged [b, S, k] (score desc, id asc)."""
+    n_shards, b, s, k = ids.shape
+    ids = ids.contiguous()
+    scores = scores.contiguous()
+    ids_out = torch.empty((b, s, k), dtype=torch.int64, device=ids.device)
+    sc_out = torch.empty((b, s, k), dtype=torch.float32, device=ids.device)
+    check(load().rcb_topk_merge_shards(_dev_ptr(ids), _dev_ptr(scores), n_shards, b, s, k,
+                                       _dev_ptr(ids_out), _dev_ptr(sc_out), _stream(stream)),
+          "rcb_topk_merge_shards")
+    return ids_out, sc_out

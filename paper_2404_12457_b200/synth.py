@@ -1,0 +1,76 @@
+"""Synthetic inputs for the hot path: embedding corpus, queries, KV contents.
+
+* Corpus embeddings are integer-valued bf16 in [-8, 8] (dim 768 by
+  default).  Every query/document inner product is then an integer below
+  2^24, exact in fp32 whatever the tensor-core accumulation order, so the
+  retrieved ids — ties included — are reproducible bit-for-bit.
+* A request's query embedding is built from its ground-truth documents (the
+  trace's doc_sequence, ragsim workload.py:124-148): solve the k x k Gram
+  system so the targets score t = (1 + 0.1*(k-1-i)) * T in relevance order,
+  scale so |q| <= 240 and round to integers (exact in bf16).  The margin to
+  random documents is ~5 sigma at 10M rows; callers verify with the oracle
+  (tests) or with the final retrieval stage (bench).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+EMB_DIM = 768
+EMB_MAX = 8
+Q_MAX = 240
+
+
+def corpus_int(n_rows: int, dim: int = EMB_DIM, seed: int = 0) -> np.ndarray:
+    """int8 [n_rows, dim] in [-EMB_MAX, EMB_MAX] (deterministic in seed)."""
+    rng = np.random.default_rng(np.random.SeedSequence([seed, 0x5EED]))
+    return rng.integers(-EMB_MAX, EMB_MAX + 1, size=(n_rows, dim), dtype=np.int8)
+
+
+def corpus_device(n_rows: int, dim: int = EMB_DIM, seed: int = 0, device="cuda",
+                  chunk: int = 1 << 20):
+    """Same distribution generated on the device (torch Philox), bf16 [n_rows, dim].
+
+    Used where the corpus is too large to ship from the host (bench sizes);
+    parity tests use corpus_int so the oracle sees identical bytes."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed) * 1_000_003 + 17)
+    out = torch.empty((n_rows, dim), dtype=torch.bfloat16, device=device)
+    for lo in range(0, n_rows, chunk):
+        hi = min(n_rows, lo + chunk)
+        out[lo:hi] = torch.randint(-EMB_MAX, EMB_MAX + 1, (hi - lo, dim), generator=g,
+                                   device=device, dtype=torch.int16).to(torch.bfloat16)
+    return out
+
+
+def target_scores(k: int) -> np.ndarray:
+    return np.array([1.0 + 0.1 * (k - 1 - i) for i in range(k)], dtype=np.float64)
+
+
+def build_query(target_rows: np.ndarray, jitter: float = 0.0,
+                rng: np.random.Generator | None = None) -> np.ndarray:
+    """Integer query (float64 holding ints, |q| <= Q_MAX) whose scores against the
+    k target rows are descending in the given order."""
+    e = target_rows.astype(np.float64)
+    k = e.shape[0]
+    t = target_scores(k)
+    if jitter and rng is not None:
+        t = t * (1.0 + jitter * rng.standard_normal(k) * 0.01)
+        t = np.sort(t)[::-1]
+    gram = e @ e.T
+    a = np.linalg.solve(gram + 1e-9 * np.eye(k), t)
+    q = a @ e
+    q *= Q_MAX / max(1e-12, np.abs(q).max())
+    return np.rint(q)
+
+
+def build_queries(corpus_rows_fn, doc_sequences, seed: int = 0) -> np.ndarray:
+    """[b, dim] integer queries; corpus_rows_fn(ids) -> int array of those rows."""
+    rng = np.random.default_rng(np.random.SeedSequence([seed, 0x0BE7]))
+    out = []
+    for docs in doc_sequences:
+        rows = corpus_rows_fn(np.asarray(docs, dtype=np.int64))
+        out.append(build_query(rows, jitter=1.0, rng=rng))
+    return np.stack(out) if out else np.zeros((0, EMB_DIM))

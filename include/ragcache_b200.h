@@ -36,6 +36,7 @@ extern "C" {
 #define RCB_SWAP_STAGED 0   /* gather kernel -> HBM staging -> cudaMemcpyAsync (and reverse) */
 #define RCB_SWAP_ZEROCOPY 1 /* gather/scatter kernel reading/writing mapped pinned host blocks */
 #define RCB_SWAP_DMA 2      /* cudaMemcpyAsync per contiguous (gpu run, host run) */
+#define RCB_POOL_ACCOUNTING 3 /* block bookkeeping only: no memory, no copies (CPU tests) */
 
 const char* rcb_last_error(void);
 int rcb_version(void);
@@ -81,6 +82,9 @@ int rcb_node_swap_in(rcb_pool* pool, const int64_t* node_keys, int32_t n);
 /* a generation's transient suffix (reserve_gpu, tree.py:320-327): one segment per
  * miss document plus one for the prompt, each block-aligned */
 int rcb_gen_reserve(rcb_pool* pool, int64_t gen_key, const int32_t* seg_tokens, int32_t nseg);
+/* free one segment early: the prompt segment at release_gpu (simulator.py:519),
+ * or a miss-doc segment whose node another commit created meanwhile */
+int rcb_gen_free_segment(rcb_pool* pool, int64_t gen_key, int32_t seg_idx);
 /* a node created by insert_path (tree.py:252-294) takes over the segment that
  * the generation's prefill already filled — no copy */
 int rcb_node_adopt(rcb_pool* pool, int64_t node_key, int64_t gen_key, int32_t seg_idx);

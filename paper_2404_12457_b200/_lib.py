@@ -28,6 +28,7 @@ RCB_TIER_HOST = 1
 RCB_SWAP_STAGED = 0
 RCB_SWAP_ZEROCOPY = 1
 RCB_SWAP_DMA = 2
+RCB_POOL_ACCOUNTING = 3
 
 
 class RcbUnavailable(RuntimeError):
@@ -60,6 +61,7 @@ SIGNATURES = [
     ("rcb_node_swap_in", c_int, [c_void_p, _p64, c_int32]),
     ("rcb_gen_reserve", c_int, [c_void_p, c_int64, _p32, c_int32]),
     ("rcb_node_adopt", c_int, [c_void_p, c_int64, c_int64, c_int32]),
+    ("rcb_gen_free_segment", c_int, [c_void_p, c_int64, c_int32]),
     ("rcb_gen_release", c_int, [c_void_p, c_int64]),
     ("rcb_node_blocks", c_int, [c_void_p, c_int64, c_int32, _p32, c_int32, _p32]),
     ("rcb_gen_blocks", c_int, [c_void_p, c_int64, c_int32, _p32, c_int32, _p32]),

@@ -19,6 +19,7 @@
 #include <functional>
 #include <queue>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "rcb_internal.h"
@@ -82,6 +83,10 @@ struct rcb_pool {
   std::unordered_map<int64_t, Gen> gens;
   int pending_dir = 0;  // 0 none, 1 gpu->host, 2 host->gpu
   std::vector<std::pair<int32_t, int32_t>> pending;  // (gpu block, host block)
+  // blocks touched by the pending batch: a batch never names a block twice, so
+  // one launch / one DMA sequence is order-free (a host block freed and reused
+  // inside a batch would otherwise race in the zero-copy kernel)
+  std::unordered_set<int32_t> pend_gpu, pend_host;
   int64_t stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
   int32_t nblocks(int32_t tokens) const { return (tokens + bt - 1) / bt; }
@@ -135,9 +140,21 @@ int issue_runs(rcb_pool* p, const std::vector<std::pair<int32_t, int32_t>>& pr, 
 }
 
 int flush(rcb_pool* p) {
+  if (p->swap_mode == RCB_POOL_ACCOUNTING) {
+    const int64_t moved = static_cast<int64_t>(p->pending.size()) * p->block_bytes;
+    if (p->pending_dir == 1) p->stats[2] += moved;
+    if (p->pending_dir == 2) p->stats[3] += moved;
+    p->pending.clear();
+    p->pend_gpu.clear();
+    p->pend_host.clear();
+    p->pending_dir = 0;
+    return RCB_OK;
+  }
   if (p->pending_dir == 0 || p->pending.empty()) {
     p->pending_dir = 0;
     p->pending.clear();
+    p->pend_gpu.clear();
+    p->pend_host.clear();
     return RCB_OK;
   }
   const bool to_host = p->pending_dir == 1;
@@ -186,17 +203,26 @@ int flush(rcb_pool* p) {
   if (to_host) p->stats[2] += moved;
   else p->stats[3] += moved;
   p->pending.clear();
+  p->pend_gpu.clear();
+  p->pend_host.clear();
   p->pending_dir = 0;
   return rc;
 }
 
 int enqueue(rcb_pool* p, int dir, const std::vector<int32_t>& g, const std::vector<int32_t>& h) {
-  if (p->pending_dir != 0 && p->pending_dir != dir) {
+  bool conflict = p->pending_dir != 0 && p->pending_dir != dir;
+  for (size_t i = 0; i < g.size() && !conflict; ++i)
+    conflict = p->pend_gpu.count(g[i]) || p->pend_host.count(h[i]);
+  if (conflict) {
     int rc = flush(p);
     if (rc != RCB_OK) return rc;
   }
   p->pending_dir = dir;
-  for (size_t i = 0; i < g.size(); ++i) p->pending.emplace_back(g[i], h[i]);
+  for (size_t i = 0; i < g.size(); ++i) {
+    p->pending.emplace_back(g[i], h[i]);
+    p->pend_gpu.insert(g[i]);
+    p->pend_host.insert(h[i]);
+  }
   return RCB_OK;
 }
 
@@ -213,7 +239,7 @@ int rcb_pool_create(int64_t num_gpu_blocks, int64_t num_host_blocks, int32_t blo
       n_kv_heads <= 0 || head_dim <= 0 || elem_bytes <= 0 || num_gpu_blocks >= (1ll << 31) ||
       num_host_blocks >= (1ll << 31))
     return set_error(RCB_ERR_ARG, "bad pool geometry");
-  if (swap_mode < RCB_SWAP_STAGED || swap_mode > RCB_SWAP_DMA)
+  if (swap_mode < RCB_SWAP_STAGED || swap_mode > RCB_POOL_ACCOUNTING)
     return set_error(RCB_ERR_ARG, "bad swap mode");
   rcb_pool* p = new rcb_pool();
   p->n_gpu = num_gpu_blocks;
@@ -229,6 +255,12 @@ int rcb_pool_create(int64_t num_gpu_blocks, int64_t num_host_blocks, int32_t blo
     return set_error(RCB_ERR_ARG, "block bytes must be a multiple of 16");
   }
   p->swap_mode = swap_mode;
+  if (swap_mode == RCB_POOL_ACCOUNTING) {
+    p->gpu_free.init(num_gpu_blocks);
+    p->host_free.init(num_host_blocks);
+    *out = p;
+    return RCB_OK;
+  }
   cudaError_t e;
   if (gpu_base != nullptr) {
     p->gpu_base = static_cast<uint8_t*>(gpu_base);
@@ -310,7 +342,8 @@ int rcb_pool_stats(rcb_pool* p, int64_t* out) {
 
 int rcb_pool_set_swap_mode(rcb_pool* p, int32_t mode) {
   if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
-  if (mode < RCB_SWAP_STAGED || mode > RCB_SWAP_DMA) return set_error(RCB_ERR_ARG, "bad mode");
+  if (mode < RCB_SWAP_STAGED || mode > RCB_SWAP_DMA || p->swap_mode == RCB_POOL_ACCOUNTING)
+    return set_error(RCB_ERR_ARG, "bad mode");
   int rc = flush(p);
   p->swap_mode = mode;
   return rc;
@@ -432,6 +465,19 @@ int rcb_node_adopt(rcb_pool* p, int64_t key, int64_t gen_key, int32_t seg_idx) {
   return RCB_OK;
 }
 
+int rcb_gen_free_segment(rcb_pool* p, int64_t gen_key, int32_t seg_idx) {
+  if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  auto git = p->gens.find(gen_key);
+  if (git == p->gens.end() || seg_idx < 0 || seg_idx >= (int32_t)git->second.segs.size())
+    return set_error(RCB_ERR_BAD_HANDLE, "unknown generation segment");
+  Seg& s = git->second.segs[seg_idx];
+  if (s.adopted) return set_error(RCB_ERR_BAD_HANDLE, "segment already adopted or freed");
+  p->gpu_free.give(s.blocks);
+  s.blocks.clear();
+  s.adopted = true;  // consumed: no longer part of the generation
+  return RCB_OK;
+}
+
 int rcb_gen_release(rcb_pool* p, int64_t gen_key) {
   if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
   auto git = p->gens.find(gen_key);
@@ -508,7 +554,7 @@ int rcb_pool_flush(rcb_pool* p) {
 int rcb_pool_fence_into(rcb_pool* p, void* stream) {
   if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
   int rc = flush(p);
-  if (rc != RCB_OK) return rc;
+  if (rc != RCB_OK || p->swap_mode == RCB_POOL_ACCOUNTING) return rc;
   cudaError_t e = cudaEventRecord(p->ev_done, p->stream);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), p->ev_done, 0);
   if (e != cudaSuccess) return set_cuda_error(e, "pool fence_into");
@@ -517,6 +563,7 @@ int rcb_pool_fence_into(rcb_pool* p, void* stream) {
 
 int rcb_pool_wait_for(rcb_pool* p, void* stream) {
   if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  if (p->swap_mode == RCB_POOL_ACCOUNTING) return RCB_OK;
   cudaError_t e = cudaEventRecord(p->ev_dep, static_cast<cudaStream_t>(stream));
   if (e == cudaSuccess) e = cudaStreamWaitEvent(p->stream, p->ev_dep, 0);
   if (e != cudaSuccess) return set_cuda_error(e, "pool wait_for");
@@ -526,7 +573,7 @@ int rcb_pool_wait_for(rcb_pool* p, void* stream) {
 int rcb_pool_sync(rcb_pool* p) {
   if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
   int rc = flush(p);
-  if (rc != RCB_OK) return rc;
+  if (rc != RCB_OK || p->swap_mode == RCB_POOL_ACCOUNTING) return rc;
   cudaError_t e = cudaStreamSynchronize(p->stream);
   if (e != cudaSuccess) return set_cuda_error(e, "pool sync");
   return RCB_OK;

@@ -8,12 +8,15 @@
 //
 // Corpus GEMM on tcgen05: A = 128 corpus rows x 64-dim atoms (TMA, SW128,
 // 5-stage ring), B = the query batch (<= 64 queries, resident in smem), D in
-// TMEM (double-buffered, 2 x NQ fp32 columns).  Epilogue (4 warps): TMEM ->
-// registers -> transposed smem tile, then each thread owns one
-// (query, row-part) pair and keeps an exact top-8 list in registers
-// (score desc, id asc).  Lists are flushed per stage segment to a workspace;
-// a merge kernel (one warp per segment, warp-shuffle argmax rounds) produces
-// the per-stage prefix top-k.  Bound: HBM (N * dim * 2 bytes per scan).
+// TMEM (double-buffered, 2 x NQ fp32 columns).  Each CTA scans a CONTIGUOUS
+// range of 128-row tiles (so it crosses at most one stage boundary).
+// Epilogue (4 warps): TMEM -> registers -> transposed smem tile, then each
+// thread owns one (query, row-part) pair and keeps an exact top-KL list in
+// registers (score desc, id asc; KL = smallest of 2/4/8 >= k).  At a stage
+// boundary the parts of a query are reduced in smem and only k entries per
+// (CTA, query) are written; a merge kernel (one warp per segment,
+// warp-shuffle argmax rounds) produces the per-stage prefix top-k.
+// Bound: HBM (N * dim * 2 bytes per scan).
 #include <cfloat>
 #include <climits>
 
@@ -36,7 +39,25 @@ struct SegInfo {
 };
 
 __device__ __forceinline__ bool better(float s1, int i1, float s2, int i2) {
-  return s1 > s2 || (s1 == s2 && i1 < i2);
+  return (s1 > s2) | ((s1 == s2) & (i1 < i2));  // bitwise: no short-circuit branches
+}
+
+// Sorted (score desc, id asc) list of KL entries in registers; insert if better
+// than the tail.  Each slot is computed from the ORIGINAL neighbours, so the
+// unrolled loop is a chain of selects.
+template <int KL>
+__device__ __forceinline__ void list_push(float (&ls)[KL], int (&li)[KL], float sc, int id) {
+  if (!better(sc, id, ls[KL - 1], li[KL - 1])) return;
+#pragma unroll
+  for (int i = KL - 1; i > 0; --i) {
+    const bool up = better(sc, id, ls[i - 1], li[i - 1]);  // e goes above slot i-1
+    const bool in = better(sc, id, ls[i], li[i]);           // e lands at or above slot i
+    ls[i] = up ? ls[i - 1] : (in ? sc : ls[i]);
+    li[i] = up ? li[i - 1] : (in ? id : li[i]);
+  }
+  const bool top = better(sc, id, ls[0], li[0]);
+  ls[0] = top ? sc : ls[0];
+  li[0] = top ? id : li[0];
 }
 
 template <int NQ>
@@ -68,10 +89,16 @@ __device__ __forceinline__ void tmem_ld_row(uint32_t taddr, float (&v)[NQ]) {
   }
 }
 
-template <int NQ>
+// The CTA's contiguous tile range [t_lo, t_hi).
+__device__ __forceinline__ void cta_tiles(int n_tiles, int& t_lo, int& t_hi) {
+  t_lo = (int)(((long long)n_tiles * blockIdx.x) / gridDim.x);
+  t_hi = (int)(((long long)n_tiles * (blockIdx.x + 1)) / gridDim.x);
+}
+
+template <int NQ, int KL>
 __global__ void __launch_bounds__(kThreads, 1)
     topk_scan_kernel(const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_q,
-                     int atoms, int n_tiles, const __grid_constant__ SegInfo seg,
+                     int atoms, int n_tiles, const __grid_constant__ SegInfo seg, int k,
                      float* __restrict__ part_score, int* __restrict__ part_id,
                      float* __restrict__ scores_out, int n_queries) {
   using Lay = Layout<NQ>;
@@ -83,8 +110,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sA = sQ + atoms * Lay::kAtomQ;
   float* sT = reinterpret_cast<float*>(sA + kStages * Lay::kA);
   uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sT) + NQ * Lay::kTStride * 4);
-  uint64_t* full = bar;                 // [kStages]
-  uint64_t* empty = bar + kStages;      // [kStages]
+  uint64_t* full = bar;                     // [kStages]
+  uint64_t* empty = bar + kStages;          // [kStages]
   uint64_t* acc_full = bar + 2 * kStages;   // [2]
   uint64_t* acc_empty = acc_full + 2;       // [2]
   uint64_t* q_full = acc_empty + 2;
@@ -111,6 +138,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  int t_lo, t_hi;
+  cta_tiles(n_tiles, t_lo, t_hi);
   auto tile_rows = [&](int t, int& sg, long long& r0, long long& r1) {
     sg = 0;
     while (sg + 1 < seg.n_seg && t >= seg.tile_begin[sg + 1]) ++sg;
@@ -126,7 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive_expect_tx(q_full, atoms * Lay::kAtomQ);
       for (int a = 0; a < atoms; ++a) tma_load_2d(sQ + a * Lay::kAtomQ, &tm_q, q_full, a * 64, 0);
       int it = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      for (int t = t_lo; t < t_hi; ++t) {
         int sg;
         long long r0, r1;
         tile_rows(t, sg, r0, r1);
@@ -146,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(q_full, 0);
       tc_fence_after();
       int it = 0, li = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++li) {
+      for (int t = t_lo; t < t_hi; ++t, ++li) {
         const int buf = li & 1;
         mbar_wait(&acc_empty[buf], ((li >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -166,32 +195,46 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // epilogue: 128 threads
+    // epilogue: 128 threads; thread = (query q, row-part)
     const int tid = threadIdx.x;
     const int q = tid % NQ;
     const int part = tid / NQ;
     const uint32_t t_row = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-    float ls[kKL];
-    int li_[kKL];
+    float ls[KL];
+    int li_[KL];
 #pragma unroll
-    for (int i = 0; i < kKL; ++i) { ls[i] = -INFINITY; li_[i] = INT_MAX; }
+    for (int i = 0; i < KL; ++i) { ls[i] = -INFINITY; li_[i] = INT_MAX; }
     int cur_seg = -1;
     unsigned flushed = 0;
-    const int P_total = gridDim.x * kParts;
+    // reduce the kParts lists of each query in smem, write k entries for this CTA
     auto flush = [&](int sg) {
-      const long long base =
-          (((long long)sg * P_total + (long long)blockIdx.x * kParts + part) * NQ + q) * kKL;
+      named_bar_sync(1, 128);  // sT free
+      float* ms = sT;                                         // [kParts][NQ][KL]
+      int* mi = reinterpret_cast<int*>(sT + kParts * NQ * KL);
 #pragma unroll
-      for (int i = 0; i < kKL; ++i) {
-        part_score[base + i] = ls[i];
-        part_id[base + i] = li_[i];
-        ls[i] = -INFINITY;
-        li_[i] = INT_MAX;
+      for (int i = 0; i < KL; ++i) {
+        ms[(part * NQ + q) * KL + i] = ls[i];
+        mi[(part * NQ + q) * KL + i] = li_[i];
       }
+      named_bar_sync(1, 128);
+      if (part == 0) {
+        for (int p = 1; p < kParts; ++p)
+#pragma unroll
+          for (int i = 0; i < KL; ++i) list_push<KL>(ls, li_, ms[(p * NQ + q) * KL + i], mi[(p * NQ + q) * KL + i]);
+        const long long base = (((long long)sg * gridDim.x + blockIdx.x) * NQ + q) * k;
+#pragma unroll
+        for (int i = 0; i < KL; ++i)
+          if (i < k) {
+            part_score[base + i] = ls[i];
+            part_id[base + i] = li_[i];
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < KL; ++i) { ls[i] = -INFINITY; li_[i] = INT_MAX; }
       flushed |= 1u << sg;
     };
     int li = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++li) {
+    for (int t = t_lo; t < t_hi; ++t, ++li) {
       int sg;
       long long r0, r1;
       tile_rows(t, sg, r0, r1);
@@ -211,32 +254,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < NQ; ++c)
           if (c < n_queries) scores_out[(r0 + tid) * n_queries + c] = v[c];
       }
+      named_bar_sync(1, 128);  // previous tile's readers are done with sT
 #pragma unroll
       for (int c = 0; c < NQ; ++c) sT[c * Lay::kTStride + tid] = v[c];
       named_bar_sync(1, 128);
       const int row_lo = part * NQ;
-      const long long nvalid = r1 - r0;
-      for (int r = 0; r < NQ; ++r) {
-        const int rr = row_lo + r;
-        if (rr >= nvalid) break;
-        const float sc = sT[q * Lay::kTStride + rr];
-        const int id = (int)(r0 + rr);
-        if (better(sc, id, ls[kKL - 1], li_[kKL - 1])) {
-          // branchless sorted insert
-          bool prev = true;  // "e is better than entry i-1" for i = 0
-#pragma unroll
-          for (int i = kKL - 1; i >= 0; --i) {
-            const bool bi = better(sc, id, ls[i], li_[i]);
-            const bool bprev = (i == 0) ? false : better(sc, id, ls[i - 1], li_[i - 1]);
-            if (bi) {
-              ls[i] = bprev ? ls[i - 1] : sc;
-              li_[i] = bprev ? li_[i - 1] : id;
-            }
-          }
-          (void)prev;
-        }
+      const int nvalid = (int)(r1 - r0);
+      const float* col = sT + q * Lay::kTStride;
+      if (row_lo + NQ <= nvalid) {
+#pragma unroll 8
+        for (int r = 0; r < NQ; ++r) list_push<KL>(ls, li_, col[row_lo + r], (int)r0 + row_lo + r);
+      } else {
+        for (int r = 0; r < NQ && row_lo + r < nvalid; ++r)
+          list_push<KL>(ls, li_, col[row_lo + r], (int)r0 + row_lo + r);
       }
-      named_bar_sync(1, 128);
     }
     if (cur_seg >= 0) flush(cur_seg);
     for (int sg = 0; sg < seg.n_seg; ++sg)
@@ -251,13 +282,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // warp-level exact top-k over candidates held as a sorted local list per lane
-__device__ __forceinline__ void warp_topk_emit(float (&ls)[kKL], int (&li)[kKL], int k,
+template <int KL>
+__device__ __forceinline__ void warp_topk_emit(float (&ls)[KL], int (&li)[KL], int k,
                                                float* out_s, int* out_i) {
-  int head = 0;
   for (int r = 0; r < k; ++r) {
-    float s = head < kKL ? ls[0] : -INFINITY;
-    int id = head < kKL ? li[0] : INT_MAX;
-    // the head is always ls[0]; entries shift down after a win
+    const float s = ls[0];
+    const int id = li[0];
     float bs = s;
     int bi = id;
 #pragma unroll
@@ -267,36 +297,25 @@ __device__ __forceinline__ void warp_topk_emit(float (&ls)[kKL], int (&li)[kKL],
       if (better(os, oi, bs, bi)) { bs = os; bi = oi; }
     }
     if (lane_id() == 0) { out_s[r] = bs; out_i[r] = bi; }
-    if (bi == id && bs == s && bi != INT_MAX) {
+    if (bi == id && bs == s && bi != INT_MAX) {  // the winner's lane pops its head
 #pragma unroll
-      for (int i = 0; i < kKL - 1; ++i) { ls[i] = ls[i + 1]; li[i] = li[i + 1]; }
-      ls[kKL - 1] = -INFINITY;
-      li[kKL - 1] = INT_MAX;
-      ++head;
+      for (int i = 0; i < KL - 1; ++i) { ls[i] = ls[i + 1]; li[i] = li[i + 1]; }
+      ls[KL - 1] = -INFINITY;
+      li[KL - 1] = INT_MAX;
     }
   }
 }
 
-__device__ __forceinline__ void list_insert(float (&ls)[kKL], int (&li)[kKL], float sc, int id) {
-  if (!better(sc, id, ls[kKL - 1], li[kKL - 1])) return;
-#pragma unroll
-  for (int i = kKL - 1; i >= 0; --i) {
-    const bool bi = better(sc, id, ls[i], li[i]);
-    const bool bprev = (i == 0) ? false : better(sc, id, ls[i - 1], li[i - 1]);
-    if (bi) {
-      ls[i] = bprev ? ls[i - 1] : sc;
-      li[i] = bprev ? li[i - 1] : id;
-    }
-  }
-}
-
-// grid = n_queries, block = 32 * n_seg; warp s reduces segment s, then emits stage s
+// grid = n_queries, block = 32 * n_seg; warp s reduces segment s (grid_scan x k
+// candidates), then emits stage s = prefix merge of segments 0..s
 __global__ void topk_merge_kernel(const float* __restrict__ part_score,
-                                  const int* __restrict__ part_id, int P_total, int NQ, int n_seg,
+                                  const int* __restrict__ part_id, int n_parts, int NQ, int n_seg,
                                   int k, long long id_offset, long long* __restrict__ ids_out,
                                   float* __restrict__ scores_out) {
   __shared__ float seg_s[kMaxSeg][kKL];
   __shared__ int seg_i[kMaxSeg][kKL];
+  __shared__ float out_s[kMaxSeg][kKL];
+  __shared__ int out_i[kMaxSeg][kKL];
   const int q = blockIdx.x;
   const int s = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -304,21 +323,18 @@ __global__ void topk_merge_kernel(const float* __restrict__ part_score,
   int li[kKL];
 #pragma unroll
   for (int i = 0; i < kKL; ++i) { ls[i] = -INFINITY; li[i] = INT_MAX; }
-  const long long n_cand = (long long)P_total * kKL;
-  for (long long c = lane; c < n_cand; c += 32) {
-    const long long p = c / kKL, e = c % kKL;
-    const long long idx = (((long long)s * P_total + p) * NQ + q) * kKL + e;
-    list_insert(ls, li, part_score[idx], part_id[idx]);
+  const int n_cand = n_parts * k;
+  for (int c = lane; c < n_cand; c += 32) {
+    const int p = c / k, e = c % k;
+    const long long idx = (((long long)s * n_parts + p) * NQ + q) * k + e;
+    list_push<kKL>(ls, li, part_score[idx], part_id[idx]);
   }
-  warp_topk_emit(ls, li, kKL, seg_s[s], seg_i[s]);
+  warp_topk_emit<kKL>(ls, li, k, seg_s[s], seg_i[s]);
   __syncthreads();
-  // stage s = prefix merge of segments 0..s
 #pragma unroll
   for (int i = 0; i < kKL; ++i) { ls[i] = -INFINITY; li[i] = INT_MAX; }
-  for (int c = lane; c < (s + 1) * kKL; c += 32) list_insert(ls, li, seg_s[c / kKL][c % kKL], seg_i[c / kKL][c % kKL]);
-  __shared__ float out_s[kMaxSeg][kKL];
-  __shared__ int out_i[kMaxSeg][kKL];
-  warp_topk_emit(ls, li, k, out_s[s], out_i[s]);
+  for (int c = lane; c < (s + 1) * k; c += 32) list_push<kKL>(ls, li, seg_s[c / k][c % k], seg_i[c / k][c % k]);
+  warp_topk_emit<kKL>(ls, li, k, out_s[s], out_i[s]);
   __syncwarp();
   if (lane < k) {
     const long long o = ((long long)q * n_seg + s) * k + lane;
@@ -415,9 +431,24 @@ int grid_for(int n_tiles) {
   return n_tiles < g ? (n_tiles > 0 ? n_tiles : 1) : g;
 }
 
+template <int NQ, int KL>
+int run_scan_kl(const CUtensorMap& tc, const CUtensorMap& tq, int atoms, int n_tiles,
+                const SegInfo& seg, int k, float* part_score, int* part_id, float* scores_out,
+                int n_queries, int grid, cudaStream_t stream) {
+  const uint32_t smem = Layout<NQ>::total(atoms);
+  auto kern = topk_scan_kernel<NQ, KL>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return set_cuda_error(e, "retrieval smem attr");
+  kern<<<grid, kThreads, smem, stream>>>(tc, tq, atoms, n_tiles, seg, k, part_score, part_id,
+                                         scores_out, n_queries);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "retrieval scan launch");
+  return RCB_OK;
+}
+
 template <int NQ>
 int run_scan(const void* corpus, int64_t n_rows, int dim, const void* queries, int n_queries,
-             int n_stages, float* part_score, int* part_id, float* scores_out, int grid,
+             int n_stages, int k, float* part_score, int* part_id, float* scores_out, int grid,
              cudaStream_t stream) {
   SegInfo seg;
   int n_tiles;
@@ -438,24 +469,20 @@ int run_scan(const void* corpus, int64_t n_rows, int dim, const void* queries, i
     if (rc != RCB_OK) return rc;
   }
   const int atoms = dim / 64;
-  const uint32_t smem = Layout<NQ>::total(atoms);
-  auto kern = topk_scan_kernel<NQ>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return set_cuda_error(e, "retrieval smem attr");
-  kern<<<grid, kThreads, smem, stream>>>(tc, tq, atoms, n_tiles, seg, part_score, part_id,
-                                         scores_out, n_queries);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return set_cuda_error(e, "retrieval scan launch");
-  return RCB_OK;
+  if (k <= 2)
+    return run_scan_kl<NQ, 2>(tc, tq, atoms, n_tiles, seg, k, part_score, part_id, scores_out, n_queries, grid, stream);
+  if (k <= 4)
+    return run_scan_kl<NQ, 4>(tc, tq, atoms, n_tiles, seg, k, part_score, part_id, scores_out, n_queries, grid, stream);
+  return run_scan_kl<NQ, 8>(tc, tq, atoms, n_tiles, seg, k, part_score, part_id, scores_out, n_queries, grid, stream);
 }
 
 int scan(const void* corpus, int64_t n_rows, int dim, const void* queries, int n_queries,
-         int n_stages, float* part_score, int* part_id, float* scores_out, int grid,
+         int n_stages, int k, float* part_score, int* part_id, float* scores_out, int grid,
          cudaStream_t stream) {
   switch (nq_pad(n_queries)) {
-    case 16: return run_scan<16>(corpus, n_rows, dim, queries, n_queries, n_stages, part_score, part_id, scores_out, grid, stream);
-    case 32: return run_scan<32>(corpus, n_rows, dim, queries, n_queries, n_stages, part_score, part_id, scores_out, grid, stream);
-    default: return run_scan<64>(corpus, n_rows, dim, queries, n_queries, n_stages, part_score, part_id, scores_out, grid, stream);
+    case 16: return run_scan<16>(corpus, n_rows, dim, queries, n_queries, n_stages, k, part_score, part_id, scores_out, grid, stream);
+    case 32: return run_scan<32>(corpus, n_rows, dim, queries, n_queries, n_stages, k, part_score, part_id, scores_out, grid, stream);
+    default: return run_scan<64>(corpus, n_rows, dim, queries, n_queries, n_stages, k, part_score, part_id, scores_out, grid, stream);
   }
 }
 
@@ -472,16 +499,15 @@ int check_args(int64_t n_rows, int dim, int n_queries, int n_stages) {
 
 using namespace rcb;
 
+// workspace: per (stage segment, scan CTA, padded query) k entries of (score, id)
 extern "C" int64_t rcb_retrieval_workspace_bytes(int64_t n_rows, int32_t n_queries, int32_t k,
                                                  int32_t n_stages) {
-  (void)k;
   ret::SegInfo seg;
   int n_tiles;
   ret::make_segments(n_rows, n_stages, seg, n_tiles);
   const int grid = ret::grid_for(n_tiles);
   const int nq = ret::nq_pad(n_queries);
-  const int64_t P_total = int64_t(grid) * (128 / nq);
-  return int64_t(n_stages) * P_total * nq * ret::kKL * 8;
+  return int64_t(n_stages) * grid * nq * (k < 1 ? 1 : k) * 8;
 }
 
 extern "C" int rcb_retrieval_topk(const void* corpus_dev, int64_t n_rows, int32_t dim,
@@ -499,14 +525,14 @@ extern "C" int rcb_retrieval_topk(const void* corpus_dev, int64_t n_rows, int32_
   ret::make_segments(n_rows, n_stages, seg, n_tiles);
   const int grid = ret::grid_for(n_tiles);
   const int nq = ret::nq_pad(n_queries);
-  const int64_t P_total = int64_t(grid) * (128 / nq);
   float* ps = static_cast<float*>(workspace_dev);
-  int* pi = reinterpret_cast<int*>(ps + int64_t(n_stages) * P_total * nq * ret::kKL);
+  int* pi = reinterpret_cast<int*>(ps + int64_t(n_stages) * grid * nq * k);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  rc = ret::scan(corpus_dev, n_rows, dim, queries_dev, n_queries, n_stages, ps, pi, nullptr, grid, st);
+  rc = ret::scan(corpus_dev, n_rows, dim, queries_dev, n_queries, n_stages, k, ps, pi, nullptr,
+                 grid, st);
   if (rc != RCB_OK) return rc;
   ret::topk_merge_kernel<<<n_queries, 32 * n_stages, 0, st>>>(
-      ps, pi, (int)P_total, nq, n_stages, k, id_offset, reinterpret_cast<long long*>(ids_out_dev),
+      ps, pi, grid, nq, n_stages, k, id_offset, reinterpret_cast<long long*>(ids_out_dev),
       scores_out_dev);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "retrieval merge launch");
@@ -518,20 +544,20 @@ extern "C" int rcb_retrieval_scores(const void* corpus_dev, int64_t n_rows, int3
                                     float* scores_out_dev, void* stream) {
   int rc = ret::check_args(n_rows, dim, n_queries, 1);
   if (rc != RCB_OK) return rc;
+  const int64_t ws = rcb_retrieval_workspace_bytes(n_rows, n_queries, 1, 1);
   ret::SegInfo seg;
   int n_tiles;
   ret::make_segments(n_rows, 1, seg, n_tiles);
   const int grid = ret::grid_for(n_tiles);
   const int nq = ret::nq_pad(n_queries);
-  const int64_t P_total = int64_t(grid) * (128 / nq);
-  const int64_t ws = P_total * nq * ret::kKL * 8;
   void* buf = nullptr;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaMallocAsync(&buf, ws, st);
   if (e != cudaSuccess) return set_cuda_error(e, "retrieval scores workspace");
   float* ps = static_cast<float*>(buf);
-  int* pi = reinterpret_cast<int*>(ps + P_total * nq * ret::kKL);
-  rc = ret::scan(corpus_dev, n_rows, dim, queries_dev, n_queries, 1, ps, pi, scores_out_dev, grid, st);
+  int* pi = reinterpret_cast<int*>(ps + int64_t(grid) * nq);
+  rc = ret::scan(corpus_dev, n_rows, dim, queries_dev, n_queries, 1, 1, ps, pi, scores_out_dev,
+                 grid, st);
   cudaFreeAsync(buf, st);
   return rc;
 }

@@ -21,27 +21,51 @@ EMB_MAX = 8
 Q_MAX = 240
 
 
-def corpus_int(n_rows: int, dim: int = EMB_DIM, seed: int = 0) -> np.ndarray:
-    """int8 [n_rows, dim] in [-EMB_MAX, EMB_MAX] (deterministic in seed)."""
-    rng = np.random.default_rng(np.random.SeedSequence([seed, 0x5EED]))
-    return rng.integers(-EMB_MAX, EMB_MAX + 1, size=(n_rows, dim), dtype=np.int8)
+_M1, _M2, _M3, _MIX = 0x27D4EB2D, 0x165667B1, 0x3C6EF372, 0x045D9F3B
+_MASK = 0xFFFFFFFF
 
 
-def corpus_device(n_rows: int, dim: int = EMB_DIM, seed: int = 0, device="cuda",
-                  chunk: int = 1 << 20):
-    """Same distribution generated on the device (torch Philox), bf16 [n_rows, dim].
+def _hash32_np(x: np.ndarray) -> np.ndarray:
+    # every product stays below 2^63 (32-bit value x 27-bit constant)
+    x = ((x ^ (x >> 16)) * _MIX) & _MASK
+    x = ((x ^ (x >> 16)) * _MIX) & _MASK
+    return x ^ (x >> 16)
 
-    Used where the corpus is too large to ship from the host (bench sizes);
-    parity tests use corpus_int so the oracle sees identical bytes."""
+
+def corpus_rows(rows: np.ndarray, dim: int = EMB_DIM, seed: int = 0) -> np.ndarray:
+    """int8 [len(rows), dim] in [-EMB_MAX, EMB_MAX]: a counter hash of (seed, row, col),
+    so any row (any shard) is reproducible on its own, on the CPU or the GPU."""
+    r = np.asarray(rows, dtype=np.int64)[:, None]
+    c = np.arange(dim, dtype=np.int64)[None, :]
+    x = (r * _M1 + c * _M2 + (seed & 0xFFFF) * _M3) & _MASK
+    return (_hash32_np(x) % (2 * EMB_MAX + 1) - EMB_MAX).astype(np.int8)
+
+
+def corpus_int(n_rows: int, dim: int = EMB_DIM, seed: int = 0, row_offset: int = 0) -> np.ndarray:
+    """Rows [row_offset, row_offset + n_rows) of the synthetic corpus."""
+    out = np.empty((n_rows, dim), dtype=np.int8)
+    step = 1 << 16
+    for lo in range(0, n_rows, step):
+        hi = min(n_rows, lo + step)
+        out[lo:hi] = corpus_rows(np.arange(row_offset + lo, row_offset + hi), dim, seed)
+    return out
+
+
+def corpus_device(n_rows: int, dim: int = EMB_DIM, seed: int = 0, row_offset: int = 0,
+                  device="cuda", chunk: int = 1 << 16):
+    """Same rows as corpus_int, generated on the device: bf16 [n_rows, dim]."""
     import torch
 
-    g = torch.Generator(device=device)
-    g.manual_seed(int(seed) * 1_000_003 + 17)
     out = torch.empty((n_rows, dim), dtype=torch.bfloat16, device=device)
+    c = torch.arange(dim, dtype=torch.int64, device=device)[None, :]
     for lo in range(0, n_rows, chunk):
         hi = min(n_rows, lo + chunk)
-        out[lo:hi] = torch.randint(-EMB_MAX, EMB_MAX + 1, (hi - lo, dim), generator=g,
-                                   device=device, dtype=torch.int16).to(torch.bfloat16)
+        r = torch.arange(row_offset + lo, row_offset + hi, dtype=torch.int64, device=device)[:, None]
+        x = (r * _M1 + c * _M2 + (seed & 0xFFFF) * _M3) & _MASK
+        x = ((x ^ (x >> 16)) * _MIX) & _MASK
+        x = ((x ^ (x >> 16)) * _MIX) & _MASK
+        x = x ^ (x >> 16)
+        out[lo:hi] = (x % (2 * EMB_MAX + 1) - EMB_MAX).to(torch.bfloat16)
     return out
 
 

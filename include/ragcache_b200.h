@@ -132,8 +132,8 @@ int rcb_kv_write_rope(const void* q, int64_t q_stride, const void* k, const void
  *   q, o        : bf16 [total_q_tokens][n_q_heads][head_dim]
  *   req_meta_dev: int32 [n_req][5] = {q_start, q_len(beta), q_pos0(alpha), blk_begin, blk_count}
  *   blk_*_dev   : int32 per block-table entry: pool block id, valid tokens, logical start pos
- *   work_dev    : int32 [n_work][4] = {req, q_tile, kv_head, n_kv_tiles}
- *                 (see rcb_attn_plan) */
+ *   work_dev    : int32 [n_work][8] = {q_start, q_len, q_pos0, blk_begin, blk_count,
+ *                 q_tile, kv_head, n_kv_tiles} (built by rcb_attn_plan, heaviest first) */
 int rcb_prefix_prefill(const void* q, void* o, int32_t total_q_tokens, int32_t n_q_heads,
                        const void* kv_pool, int64_t num_pool_blocks, int32_t block_tokens,
                        int32_t n_layers, int32_t n_kv_heads, int32_t head_dim, int32_t layer,
@@ -141,7 +141,7 @@ int rcb_prefix_prefill(const void* q, void* o, int32_t total_q_tokens, int32_t n
                        const int32_t* blk_valid_dev, const int32_t* blk_pos_dev,
                        const int32_t* work_dev, int32_t n_work, float softmax_scale,
                        void* stream);
-/* host-side work planner for rcb_prefix_prefill: writes up to cap items into
+/* host-side work planner for rcb_prefix_prefill: writes up to cap items (8 int32 each) into
  * work_out (heaviest first) and returns the count in n_work_out.  Inputs are the
  * host copies of req_meta / blk_valid / blk_pos. */
 int rcb_attn_plan(const int32_t* req_meta, int32_t n_req, const int32_t* blk_valid,

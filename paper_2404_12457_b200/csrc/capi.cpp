@@ -81,7 +81,8 @@ int rcb_prefix_prefill(const void* q, void* o, int32_t total_q_tokens, int32_t n
                              softmax_scale, static_cast<cudaStream_t>(stream));
 }
 
-// Work items (req, q_tile, kv_head, n_kv_tiles).  A query tile only needs the
+// Work items {q_start, q_len, q_pos0, blk_begin, blk_count, q_tile, kv_head,
+// n_kv_tiles} (self-contained so the kernel never chases req_meta).  A query tile only needs the
 // key tiles up to the slot holding its last query position (causal), so the
 // count is found by a binary search over the table's logical block starts.
 // Items are ordered heaviest-first so long tiles start in the first wave.
@@ -95,6 +96,7 @@ int rcb_attn_plan(const int32_t* req_meta, int32_t n_req, const int32_t* blk_val
   struct Item {
     int32_t r, qt, h, tiles;
   };
+  const int kItemInts = 8;
   std::vector<Item> items;
   for (int32_t r = 0; r < n_req; ++r) {
     const int32_t q_len = req_meta[r * 5 + 1];
@@ -125,10 +127,16 @@ int rcb_attn_plan(const int32_t* req_meta, int32_t n_req, const int32_t* blk_val
   if (static_cast<int32_t>(items.size()) > cap)
     return rcb::set_error(RCB_ERR_ARG, "work capacity too small");
   for (size_t i = 0; i < items.size(); ++i) {
-    work_out[4 * i + 0] = items[i].r;
-    work_out[4 * i + 1] = items[i].qt;
-    work_out[4 * i + 2] = items[i].h;
-    work_out[4 * i + 3] = items[i].tiles;
+    const int32_t* m = req_meta + items[i].r * 5;
+    int32_t* w = work_out + kItemInts * i;
+    w[0] = m[0];  // q_start
+    w[1] = m[1];  // q_len
+    w[2] = m[2];  // q_pos0
+    w[3] = m[3];  // blk_begin
+    w[4] = m[4];  // blk_count
+    w[5] = items[i].qt;
+    w[6] = items[i].h;
+    w[7] = items[i].tiles;
   }
   return RCB_OK;
 }

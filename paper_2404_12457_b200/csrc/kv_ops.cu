@@ -95,7 +95,31 @@ int copy_grid(int64_t block_bytes, int n) {
 }
 
 // ------------------------------------------------------------------ RoPE + write
-__global__ void __launch_bounds__(256)
+// One CTA per token.  cos/sin of the token's head_dim/2 frequencies are
+// computed once into shared memory and shared by every q/k head; each thread
+// then rotates 8-element (16 B) chunks of x[i] and x[i + d/2] and copies V
+// chunks straight into the token's pool slot.
+constexpr int kRopeThreads = 128;
+
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return u;
+}
+
+__global__ void __launch_bounds__(kRopeThreads)
     kv_write_rope_kernel(const __nv_bfloat16* __restrict__ q, int64_t q_stride,
                          const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
                          int64_t kv_stride, __nv_bfloat16* __restrict__ q_out,
@@ -103,9 +127,14 @@ __global__ void __launch_bounds__(256)
                          int n_q_heads, __nv_bfloat16* __restrict__ pool, int block_tokens,
                          int64_t block_elems, int n_kv_heads, int head_dim, int layer,
                          float log2_theta) {
+  __shared__ float s_cos[128], s_sin[128];
   const int t = blockIdx.x;
   const int half = head_dim / 2;
   const float pos = static_cast<float>(positions[t]);
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {
+    const float inv_freq = exp2f(-(2.f * i / head_dim) * log2_theta);
+    sincosf(pos * inv_freq, &s_sin[i], &s_cos[i]);
+  }
   const int slot = slots[t];
   const int blk = slot / block_tokens;
   const int off = slot - blk * block_tokens;
@@ -113,37 +142,40 @@ __global__ void __launch_bounds__(256)
   __nv_bfloat16* kbase = pool + int64_t(blk) * block_elems +
                          int64_t(2 * layer) * n_kv_heads * tile + int64_t(off) * head_dim;
   __nv_bfloat16* vbase = kbase + int64_t(n_kv_heads) * tile;
-  const int rot_items = (n_q_heads + n_kv_heads) * half;
-  const int total = rot_items + n_kv_heads * half;
-  for (int it = threadIdx.x; it < total; it += blockDim.x) {
-    if (it < rot_items) {
-      const int h = it / half;
-      const int i = it - h * half;
-      const float inv_freq = exp2f(-(2.f * i / head_dim) * log2_theta);
-      float sn, cs;
-      sincosf(pos * inv_freq, &sn, &cs);
+  __syncthreads();
+  const int cph = half / 8;  // 16-byte chunks per half row
+  const int rot_units = (n_q_heads + n_kv_heads) * cph;
+  const int v_units = n_kv_heads * (head_dim / 8);
+  for (int u = threadIdx.x; u < rot_units + v_units; u += blockDim.x) {
+    if (u < rot_units) {
+      const int h = u / cph;
+      const int c = (u - h * cph) * 8;
       const __nv_bfloat16* src;
       __nv_bfloat16* dst;
       if (h < n_q_heads) {
         src = q + int64_t(t) * q_stride + int64_t(h) * head_dim;
         dst = q_out + (int64_t(t) * n_q_heads + h) * head_dim;
       } else {
-        const int kh = h - n_q_heads;
-        src = k + int64_t(t) * kv_stride + int64_t(kh) * head_dim;
-        dst = kbase + int64_t(kh) * tile;
+        src = k + int64_t(t) * kv_stride + int64_t(h - n_q_heads) * head_dim;
+        dst = kbase + int64_t(h - n_q_heads) * tile;
       }
-      const float x0 = __bfloat162float(src[i]);
-      const float x1 = __bfloat162float(src[i + half]);
-      dst[i] = __float2bfloat16(x0 * cs - x1 * sn);
-      dst[i + half] = __float2bfloat16(x1 * cs + x0 * sn);
+      float x0[8], x1[8], y0[8], y1[8];
+      unpack8(*reinterpret_cast<const uint4*>(src + c), x0);
+      unpack8(*reinterpret_cast<const uint4*>(src + c + half), x1);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float cs = s_cos[c + e], sn = s_sin[c + e];
+        y0[e] = x0[e] * cs - x1[e] * sn;
+        y1[e] = x1[e] * cs + x0[e] * sn;
+      }
+      *reinterpret_cast<uint4*>(dst + c) = pack8(y0);
+      *reinterpret_cast<uint4*>(dst + c + half) = pack8(y1);
     } else {
-      const int j = it - rot_items;
-      const int h = j / half;
-      const int i = j - h * half;
-      const __nv_bfloat16* src = v + int64_t(t) * kv_stride + int64_t(h) * head_dim;
-      __nv_bfloat16* dst = vbase + int64_t(h) * tile;
-      dst[i] = src[i];
-      dst[i + half] = src[i + half];
+      const int j = u - rot_units;
+      const int h = j / (head_dim / 8);
+      const int c = (j - h * (head_dim / 8)) * 8;
+      *reinterpret_cast<uint4*>(vbase + int64_t(h) * tile + c) =
+          *reinterpret_cast<const uint4*>(v + int64_t(t) * kv_stride + int64_t(h) * head_dim + c);
     }
   }
 }
@@ -188,10 +220,12 @@ extern "C" int rcb_kv_write_rope(const void* q, int64_t q_stride, const void* k,
                                  int32_t n_kv_heads, int32_t head_dim, int32_t layer,
                                  float rope_theta, void* stream) {
   if (n_tokens == 0) return RCB_OK;
-  if (head_dim % 2 != 0 || layer < 0 || layer >= n_layers)
-    return rcb::set_error(RCB_ERR_ARG, "bad head_dim or layer");
+  if (head_dim % 16 != 0 || head_dim > 256 || layer < 0 || layer >= n_layers)
+    return rcb::set_error(RCB_ERR_ARG, "head_dim must be a multiple of 16 (<= 256), layer in range");
+  if (q_stride % 8 != 0 || kv_stride % 8 != 0)
+    return rcb::set_error(RCB_ERR_ARG, "q/kv row strides must be multiples of 8 elements");
   const int64_t block_elems = int64_t(n_layers) * 2 * n_kv_heads * block_tokens * head_dim;
-  rcb::kv_write_rope_kernel<<<n_tokens, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  rcb::kv_write_rope_kernel<<<n_tokens, rcb::kRopeThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const __nv_bfloat16*>(q), q_stride, static_cast<const __nv_bfloat16*>(k),
       static_cast<const __nv_bfloat16*>(v), kv_stride, static_cast<__nv_bfloat16*>(q_out),
       positions_dev, slots_dev, n_q_heads, static_cast<__nv_bfloat16*>(kv_pool), block_tokens,

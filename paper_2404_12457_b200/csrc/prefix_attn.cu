@@ -6,13 +6,15 @@
 // blocks through a block table, and only the beta suffix tokens (miss docs +
 // prompt) are computed as queries.
 //
-// One CTA = one work item (request, query tile, kv head):
+// Persistent CTAs (one per SM) walk a heaviest-first list of work items
+// (request, query tile, kv head), pipelining across items:
 //   * 128 query rows = (128/G tokens) x (G query heads sharing the kv head)
 //   * K/V tiles of 128 key slots = 128/BT pool blocks, TMA-loaded (SW128)
 //   * S = Q K^T and O += P V on tcgen05 (fp32 accumulators in TMEM)
 //   * online softmax in registers, one thread per row (warps 0-3),
 //     lazily rescaled O (only when the running max grows by > 2^8)
-// Warp roles: 0-3 softmax/epilogue, 4 TMA producer, 5 MMA issuer + TMEM owner.
+// Warp roles: 0-3 softmax/epilogue, 4 Q/K TMA producer, 5 MMA issuer + TMEM
+// owner, 6 V TMA producer.
 //
 // Key slots carry holes (node tails: a block holds `valid` <= BT tokens), so
 // each block also carries its logical start position; a slot is attended iff
@@ -24,38 +26,54 @@ namespace rcb {
 
 namespace attn {
 
-constexpr int kThreads = 192;
+// WG0 (warps 0-3) softmax | WG1: warp 4 Q+K producer, 5 MMA, 6 V producer, 7 idle |
+// WG2 (warps 8-11) epilogue.  setmaxnreg moves registers to the softmax WG.
+constexpr int kThreads = 384;
 constexpr int kRows = 128;
 constexpr int kKeys = 128;  // key slots per KV tile
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
-template <int HD>
+template <int HD, int BT>
 struct Smem {
   static constexpr uint32_t kHalves = HD / 64;
-  static constexpr uint32_t kQ = kHalves * 16384;
+  static constexpr uint32_t kQ = kHalves * 16384;   // one Q tile
   static constexpr uint32_t kKV = kHalves * 16384;  // one K or V stage
   static constexpr uint32_t kP = 2 * 16384;
-  static constexpr uint32_t offQ = 0;
-  static constexpr uint32_t offK = offQ + kQ;
-  static constexpr uint32_t offV = offK + 2 * kKV;
+  static constexpr int kBPT = kKeys / BT;
+  static constexpr uint32_t offQ = 0;                // [2]
+  static constexpr uint32_t offK = offQ + 2 * kQ;    // [2]
+  static constexpr uint32_t offV = offK + 2 * kKV;   // [2]
   static constexpr uint32_t offP = offV + 2 * kKV;
-  static constexpr uint32_t offBar = offP + kP;
-  static constexpr uint32_t kTotal = offBar + 256 + 1024;  // + alignment slack
+  static constexpr int kMetaSlots = 4;
+  static constexpr uint32_t offMeta = offP + kP;     // int [kMetaSlots][2][kBPT]
+  static constexpr uint32_t offL = offMeta + kMetaSlots * 2 * kBPT * 4;  // float [2][128]
+  static constexpr uint32_t offBar = offL + 2 * 128 * 4;
+  static constexpr uint32_t kTotal = offBar + 32 * 8 + 16 + 1024;  // + alignment slack
 };
 
 enum Bar {
-  kQFull = 0,
-  kKFull0 = 1,
-  kVFull0 = 3,
-  kKVEmpty0 = 5,
-  kSFull0 = 7,
-  kSFree0 = 9,
-  kPFull = 11,
-  kPFree = 12,
-  kOFull = 13,
-  kNumBars = 14
+  kQFull0 = 0, kQEmpty0 = 2, kKFull0 = 4, kVFull0 = 6, kKEmpty0 = 8, kSFull0 = 10, kSFree0 = 12,
+  kPFull = 14, kPFree = 15, kOFull0 = 16, kOFree0 = 18, kVEmpty0 = 20, kMetaFull0 = 22,
+  kMetaFree0 = 26, kLFull0 = 30, kNumBars = 32
 };
 
+// Work items are self-contained (no dependent loads at item start):
+//   {q_start, q_len, q_pos0, blk_begin, blk_count, q_tile, kv_head, n_kv_tiles}
+constexpr int kItemInts = 8;
+struct Item {
+  int q_start, q_len, q_pos0, blk_begin, blk_count, qt, kvh, n;
+};
+
+__device__ __forceinline__ Item load_item(const int* __restrict__ work, int idx) {
+  const int4 a = *reinterpret_cast<const int4*>(work + idx * kItemInts);
+  const int4 b = *reinterpret_cast<const int4*>(work + idx * kItemInts + 4);
+  return Item{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+}
+
+// Persistent: CTA c serves work items c, c + grid, ... (heaviest first).
+// Per-CTA tile sequence number g runs across items, so K/V stages, S buffers
+// and the P handshake keep their phase; Q (smem) and O (TMEM) are double
+// buffered per item so item i's epilogue overlaps item i+1's first tiles.
 template <int HD, int G, int BT>
 __global__ void __launch_bounds__(kThreads, 1)
     prefix_prefill_kernel(const __grid_constant__ CUtensorMap tm_q,
@@ -63,44 +81,45 @@ __global__ void __launch_bounds__(kThreads, 1)
                           __nv_bfloat16* __restrict__ out, int n_q_heads, int layer,
                           const int* __restrict__ req_meta, const int* __restrict__ blk_ids,
                           const int* __restrict__ blk_valid, const int* __restrict__ blk_pos,
-                          const int* __restrict__ work, float scale_log2) {
-  using S = Smem<HD>;
+                          const int* __restrict__ work, int n_work, float scale_log2) {
+  using S = Smem<HD, BT>;
   constexpr int TQ = kRows / G;
-  constexpr int BPT = kKeys / BT;  // pool blocks per KV tile
+  constexpr int BPT = S::kBPT;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // align within the shared window without leaving the shared address space
+  // (keeps st.shared / ld.shared instead of generic accesses)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem + S::offQ;
   uint8_t* sK = smem + S::offK;
   uint8_t* sV = smem + S::offV;
   uint8_t* sP = smem + S::offP;
+  int* sMeta = reinterpret_cast<int*>(smem + S::offMeta);  // [slot][0=valid,1=pos][BPT]
+  float* sL = reinterpret_cast<float*>(smem + S::offL);    // [ob][row] softmax row sums
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::offBar);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + kNumBars);
 
   const int warp = threadIdx.x >> 5;
-  const int item = blockIdx.x;
-  const int req = work[item * 4 + 0];
-  const int qt = work[item * 4 + 1];
-  const int kvh = work[item * 4 + 2];
-  const int n_tiles = work[item * 4 + 3];
-  const int q_start = req_meta[req * 5 + 0];
-  const int q_len = req_meta[req * 5 + 1];
-  const int q_pos0 = req_meta[req * 5 + 2];
-  const int blk_begin = req_meta[req * 5 + 3];
-  const int blk_count = req_meta[req * 5 + 4];
-
   if (threadIdx.x == 0) {
-    mbar_init(&bar[kQFull], 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&bar[kKFull0 + s], 1);
-      mbar_init(&bar[kVFull0 + s], 1);
-      mbar_init(&bar[kKVEmpty0 + s], 1);
-      mbar_init(&bar[kSFull0 + s], 1);
-      mbar_init(&bar[kSFree0 + s], kRows);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bar[kQFull0 + b], 1);
+      mbar_init(&bar[kQEmpty0 + b], 1);
+      mbar_init(&bar[kKFull0 + b], 1);
+      mbar_init(&bar[kVFull0 + b], 1);
+      mbar_init(&bar[kKEmpty0 + b], 1);
+      mbar_init(&bar[kVEmpty0 + b], 1);
+      mbar_init(&bar[kSFull0 + b], 1);
+      mbar_init(&bar[kSFree0 + b], kRows);
+      mbar_init(&bar[kOFull0 + b], 1);
+      mbar_init(&bar[kOFree0 + b], kRows);
     }
     mbar_init(&bar[kPFull], kRows);
     mbar_init(&bar[kPFree], 1);
-    mbar_init(&bar[kOFull], 1);
+    for (int b = 0; b < S::kMetaSlots; ++b) {
+      mbar_init(&bar[kMetaFull0 + b], 1);
+      mbar_init(&bar[kMetaFree0 + b], kRows);
+    }
+    mbar_init(&bar[kLFull0 + 0], kRows);
+    mbar_init(&bar[kLFull0 + 1], kRows);
     fence_barrier_init();
   }
   if (warp == 5) tmem_alloc<512>(tmem_slot);
@@ -109,36 +128,71 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  if (warp >= 4 && warp < 8) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+  }
   if (warp == 4) {
     // ------------------------------------------------------------ TMA producer
     if (elect_one()) {
       tma_prefetch(&tm_q);
       tma_prefetch(&tm_kv);
-      mbar_arrive_expect_tx(&bar[kQFull], S::kQ);
-      for (int h = 0; h < (int)S::kHalves; ++h)
-        tma_load_3d(sQ + h * 16384, &tm_q, &bar[kQFull], h * 64, kvh * G, q_start + qt * TQ);
-      for (int j = 0; j < n_tiles; ++j) {
-        const int st = j & 1;
-        mbar_wait(&bar[kKVEmpty0 + st], ((j >> 1) & 1) ^ 1);
-        int ids[BPT];
+      int g = 0;
+      for (int idx = blockIdx.x, ii = 0; idx < n_work; idx += gridDim.x, ++ii) {
+        const Item it = load_item(work, idx);
+        const int qb = ii & 1;
+        mbar_wait(&bar[kQEmpty0 + qb], ((ii >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&bar[kQFull0 + qb], S::kQ);
+        for (int h = 0; h < (int)S::kHalves; ++h)
+          tma_load_3d(sQ + qb * S::kQ + h * 16384, &tm_q, &bar[kQFull0 + qb], h * 64,
+                      it.kvh * G, it.q_start + it.qt * TQ);
+        for (int j = 0; j < it.n; ++j, ++g) {
+          const int st = g & 1;
+          // per-tile mask metadata: its own 4-slot ring (the softmax may lag the K ring)
+          const int ms = g & (S::kMetaSlots - 1);
+          mbar_wait(&bar[kMetaFree0 + ms], ((g / S::kMetaSlots) & 1) ^ 1);
+          int ids[BPT];
 #pragma unroll
-        for (int b = 0; b < BPT; ++b) {
-          const int sb = j * BPT + b;
-          // slots past the table load a real (finite) block; they are masked
-          ids[b] = blk_ids[blk_begin + (sb < blk_count ? sb : 0)];
+          for (int b = 0; b < BPT; ++b) {
+            const int sb = j * BPT + b;
+            const bool in = sb < it.blk_count;
+            // slots past the table load a real (finite) block; they are masked
+            ids[b] = blk_ids[it.blk_begin + (in ? sb : 0)];
+            sMeta[(ms * 2 + 0) * BPT + b] = in ? blk_valid[it.blk_begin + sb] : 0;
+            sMeta[(ms * 2 + 1) * BPT + b] = in ? blk_pos[it.blk_begin + sb] : 0;
+          }
+          mbar_arrive(&bar[kMetaFull0 + ms]);  // release: publishes sMeta[ms]
+          mbar_wait(&bar[kKEmpty0 + st], ((g >> 1) & 1) ^ 1);  // QK(g-2) retired
+          mbar_arrive_expect_tx(&bar[kKFull0 + st], S::kKV);
+#pragma unroll
+          for (int b = 0; b < BPT; ++b)
+            for (int h = 0; h < (int)S::kHalves; ++h)
+              tma_load_5d(sK + st * S::kKV + h * 16384 + b * BT * 128, &tm_kv,
+                          &bar[kKFull0 + st], h * 64, 0, it.kvh, 2 * layer, ids[b]);
         }
-        mbar_arrive_expect_tx(&bar[kKFull0 + st], S::kKV);
+      }
+    }
+  } else if (warp == 6) {
+    // ------------------------------------------------------------ V producer
+    // V(g) is only needed by PV(g); its stage frees when PV(g) retires, while K
+    // stages free as soon as QK(g) retires — separate rings keep both ahead.
+    if (elect_one()) {
+      int g = 0;
+      for (int idx = blockIdx.x; idx < n_work; idx += gridDim.x) {
+        const Item it = load_item(work, idx);
+        const int n = it.n, kvh = it.kvh, blk_begin = it.blk_begin, blk_count = it.blk_count;
+        for (int j = 0; j < n; ++j, ++g) {
+          const int st = g & 1;
+          mbar_wait(&bar[kVEmpty0 + st], ((g >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&bar[kVFull0 + st], S::kKV);
 #pragma unroll
-        for (int b = 0; b < BPT; ++b)
-          for (int h = 0; h < (int)S::kHalves; ++h)
-            tma_load_5d(sK + st * S::kKV + h * 16384 + b * BT * 128, &tm_kv, &bar[kKFull0 + st],
-                        h * 64, 0, kvh, 2 * layer, ids[b]);
-        mbar_arrive_expect_tx(&bar[kVFull0 + st], S::kKV);
-#pragma unroll
-        for (int b = 0; b < BPT; ++b)
-          for (int h = 0; h < (int)S::kHalves; ++h)
-            tma_load_5d(sV + st * S::kKV + h * 16384 + b * BT * 128, &tm_kv, &bar[kVFull0 + st],
-                        h * 64, 0, kvh, 2 * layer + 1, ids[b]);
+          for (int b = 0; b < BPT; ++b) {
+            const int sb = j * BPT + b;
+            const int id = blk_ids[blk_begin + (sb < blk_count ? sb : 0)];
+            for (int h = 0; h < (int)S::kHalves; ++h)
+              tma_load_5d(sV + st * S::kKV + h * 16384 + b * BT * 128, &tm_kv,
+                          &bar[kVFull0 + st], h * 64, 0, kvh, 2 * layer + 1, id);
+          }
+        }
       }
     }
   } else if (warp == 5) {
@@ -150,165 +204,249 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t k_base = smem_u32(sK);
       const uint32_t v_base = smem_u32(sV);
       const uint32_t p_base = smem_u32(sP);
-      mbar_wait(&bar[kQFull], 0);
-      tc_fence_after();
-      auto issue_qk = [&](int j) {
-        const int st = j & 1;
-        mbar_wait(&bar[kKFull0 + st], (j >> 1) & 1);
-        mbar_wait(&bar[kSFree0 + st], ((j >> 1) & 1) ^ 1);
+      struct T {
+        int idx, ii, j, n, g;
+      };
+      auto first = [&](T& t) {
+        t.idx = blockIdx.x;
+        t.ii = 0;
+        t.j = 0;
+        t.g = 0;
+        t.n = (t.idx < n_work) ? work[t.idx * kItemInts + 7] : 0;
+      };
+      auto next = [&](T t) {
+        ++t.g;
+        if (++t.j == t.n) {
+          t.j = 0;
+          ++t.ii;
+          t.idx += gridDim.x;
+          t.n = (t.idx < n_work) ? work[t.idx * kItemInts + 7] : 0;
+        }
+        return t;
+      };
+      auto issue_qk = [&](const T& t) {
+        const int qb = t.ii & 1;
+        const int st = t.g & 1;
+        if (t.j == 0) mbar_wait(&bar[kQFull0 + qb], (t.ii >> 1) & 1);
+        mbar_wait(&bar[kKFull0 + st], (t.g >> 1) & 1);
+        mbar_wait(&bar[kSFree0 + st], ((t.g >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + st * kKeys;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          const uint64_t a = sw128_desc(q_base + off, 16, 1024);
+          const uint64_t a = sw128_desc(q_base + qb * S::kQ + off, 16, 1024);
           const uint64_t b = sw128_desc(k_base + st * S::kKV + off, 16, 1024);
           umma_bf16_ss(d, a, b, idesc_qk, kk > 0 ? 1u : 0u);
         }
         umma_commit(&bar[kSFull0 + st]);
+        umma_commit(&bar[kKEmpty0 + st]);                       // K stage no longer read
+        if (t.j == t.n - 1) umma_commit(&bar[kQEmpty0 + qb]);  // Q tile no longer read
       };
-      issue_qk(0);
-      for (int j = 0; j < n_tiles; ++j) {
-        if (j + 1 < n_tiles) issue_qk(j + 1);
-        const int st = j & 1;
-        mbar_wait(&bar[kPFull], j & 1);
-        mbar_wait(&bar[kVFull0 + st], (j >> 1) & 1);
+      auto issue_pv = [&](const T& t) {
+        const int ob = t.ii & 1;
+        const int st = t.g & 1;
+        if (t.j == 0) mbar_wait(&bar[kOFree0 + ob], ((t.ii >> 1) & 1) ^ 1);
+        mbar_wait(&bar[kPFull], t.g & 1);
+        mbar_wait(&bar[kVFull0 + st], (t.g >> 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < kKeys / 16; ++kk) {
           const uint64_t a = sw128_desc(p_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
           // V tile is [half][128 keys][64]: MN-major, halves 16 KB apart (LBO)
           const uint64_t b = sw128_desc(v_base + st * S::kKV + kk * 2048, 16384, 1024);
-          umma_bf16_ss(tmem + 256, a, b, idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+          umma_bf16_ss(tmem + 256 + ob * 128, a, b, idesc_pv, (t.j > 0 || kk > 0) ? 1u : 0u);
         }
-        umma_commit(&bar[kKVEmpty0 + st]);
+        umma_commit(&bar[kVEmpty0 + st]);
         umma_commit(&bar[kPFree]);
+        if (t.j == t.n - 1) umma_commit(&bar[kOFull0 + ob]);
+      };
+      T cur;
+      first(cur);
+      if (cur.n > 0) {
+        issue_qk(cur);
+        while (true) {
+          const T nx = next(cur);
+          const bool more = nx.n > 0;
+          if (more) issue_qk(nx);  // next QK (possibly the next item's) before this PV
+          issue_pv(cur);
+          if (!more) break;
+          cur = nx;
+        }
       }
-      umma_commit(&bar[kOFull]);
     }
-  } else {
+  } else if (warp < 4) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 248;\n" ::: "memory");
     // ------------------------------------------------------------ softmax rows
     const int row = threadIdx.x;  // == TMEM lane
     const int t_local = row / G;
     const int h_local = row % G;
-    const int tok = qt * TQ + t_local;
-    const bool row_valid = tok < q_len;
-    const int qp = q_pos0 + tok;
     const uint32_t t_row = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-    float m = -INFINITY;  // running max (scaled, log2 domain); may be stale by < 2^8
-    float l = 0.f;
     float s[kKeys];
-    for (int j = 0; j < n_tiles; ++j) {
-      // tile metadata (broadcast loads)
-      int vv[BPT], pp[BPT];
-      bool all_valid = true;
-      int max_pos = -1;
+    int g = 0;
+    const uint32_t p_row_addr = smem_u32(sP) + (row >> 3) * 1024 + (row & 7) * 128;
+    for (int idx = blockIdx.x, ii = 0; idx < n_work; idx += gridDim.x, ++ii) {
+      const Item it = load_item(work, idx);
+      const int ob = ii & 1;
+      const int tok = it.qt * TQ + t_local;
+      const bool row_valid = tok < it.q_len;
+      const int qp = it.q_pos0 + tok;
+      float m = -INFINITY;  // running max (scaled, log2 domain); may be stale by < 2^8
+      float l = 0.f;
+      for (int j = 0; j < it.n; ++j, ++g) {
+        const int st = g & 1;
+        const int ms = g & (S::kMetaSlots - 1);
+        mbar_wait(&bar[kMetaFull0 + ms], (g / S::kMetaSlots) & 1);
+        int vv[BPT], pp[BPT];
+        bool all_valid = true;
+        int max_pos = -1;
 #pragma unroll
-      for (int b = 0; b < BPT; ++b) {
-        const int sb = j * BPT + b;
-        const bool in = sb < blk_count;
-        vv[b] = in ? blk_valid[blk_begin + sb] : 0;
-        pp[b] = in ? blk_pos[blk_begin + sb] : 0;
-        all_valid &= (vv[b] == BT);
-        max_pos = max(max_pos, pp[b] + vv[b] - 1);
-      }
-      const int st = j & 1;
-      mbar_wait(&bar[kSFull0 + st], (j >> 1) & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < kKeys / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(t_row + st * kKeys + c * 32, r);
-        tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);
-      }
-      tc_fence_before();
-      mbar_arrive(&bar[kSFree0 + st]);
-
-      if (!all_valid || max_pos > qp) {
-#pragma unroll
-        for (int c = 0; c < kKeys; ++c) {
-          const int b = c / BT, off = c % BT;
-          const bool ok = off < vv[b] && pp[b] + off <= qp;
-          s[c] = ok ? s[c] : -INFINITY;
+        for (int b = 0; b < BPT; ++b) {
+          vv[b] = sMeta[(ms * 2 + 0) * BPT + b];
+          pp[b] = sMeta[(ms * 2 + 1) * BPT + b];
+          all_valid &= (vv[b] == BT);
+          max_pos = max(max_pos, pp[b] + vv[b] - 1);
         }
-      }
-      float tmax = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < kKeys; ++c) tmax = fmaxf(tmax, s[c]);
-      tmax *= scale_log2;
-      float alpha = 1.f;
-      bool rescale = false;
-      if (j == 0) {
-        m = (tmax == -INFINITY) ? 0.f : tmax;
-      } else if (tmax > m + kRescaleThreshold) {
-        alpha = exp2f(m - tmax);
-        m = tmax;
-        l *= alpha;
-        rescale = true;
-      }
-      float rs = 0.f;
-#pragma unroll
-      for (int c = 0; c < kKeys; ++c) {
-        const float p = exp2f(fmaf(s[c], scale_log2, -m));
-        s[c] = p;
-        rs += p;
-      }
-      l += rs;
-      if (j > 0) {
-        mbar_wait(&bar[kPFree], (j - 1) & 1);
+        mbar_arrive(&bar[kMetaFree0 + ms]);
+        mbar_wait(&bar[kSFull0 + st], (g >> 1) & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, rescale)) {
+#pragma unroll
+        for (int c = 0; c < kKeys / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(t_row + st * kKeys + c * 32, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);
+        }
+        tc_fence_before();
+        mbar_arrive(&bar[kSFree0 + st]);
+
+        if (!all_valid || max_pos > qp) {
+          // keys valid in block b for this row: off < min(valid_b, qp - pos_b + 1)
+          int lim[BPT];
+#pragma unroll
+          for (int b = 0; b < BPT; ++b) lim[b] = min(vv[b], qp - pp[b] + 1);
+#pragma unroll
+          for (int c = 0; c < kKeys; ++c) s[c] = (c % BT) < lim[c / BT] ? s[c] : -INFINITY;
+        }
+        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < kKeys; c += 8) {
+          mx0 = fmax3(mx0, s[c + 0], s[c + 1]);
+          mx1 = fmax3(mx1, s[c + 2], s[c + 3]);
+          mx2 = fmax3(mx2, s[c + 4], s[c + 5]);
+          mx3 = fmax3(mx3, s[c + 6], s[c + 7]);
+        }
+        float tmax = fmax3(fmaxf(mx0, mx1), mx2, mx3) * scale_log2;
+        float alpha = 1.f;
+        bool rescale = false;
+        if (j == 0) {
+          m = (tmax == -INFINITY) ? 0.f : tmax;
+        } else if (tmax > m + kRescaleThreshold) {
+          alpha = ex2_mufu(m - tmax);
+          m = tmax;
+          l *= alpha;
+          rescale = true;
+        }
+        // p = 2^(s*scale - m): packed FFMA2, MUFU for 6 of every 8 columns and the
+        // FMA-pipe polynomial for the other 2; row sum with packed FADD2
+        const uint64_t sc2 = f2_pack(scale_log2, scale_log2);
+        const uint64_t nm2 = f2_pack(-m, -m);
+        uint64_t acc0 = f2_pack(0.f, 0.f), acc1 = acc0;
+#pragma unroll
+        for (int c = 0; c < kKeys; c += 8) {
+          float x[8];
+#pragma unroll
+          for (int e = 0; e < 8; e += 2) f2_unpack(ffma2(f2_pack(s[c + e], s[c + e + 1]), sc2, nm2), x[e], x[e + 1]);
+#pragma unroll
+          for (int e = 0; e < 6; ++e) s[c + e] = ex2_mufu(x[e]);
+          f2_unpack(ex2_poly2(x[6], x[7]), s[c + 6], s[c + 7]);
+          acc0 = fadd2(acc0, f2_pack(s[c + 0], s[c + 1]));
+          acc1 = fadd2(acc1, f2_pack(s[c + 2], s[c + 3]));
+          acc0 = fadd2(acc0, f2_pack(s[c + 4], s[c + 5]));
+          acc1 = fadd2(acc1, f2_pack(s[c + 6], s[c + 7]));
+        }
+        float a0, a1, b0, b1;
+        f2_unpack(acc0, a0, a1);
+        f2_unpack(acc1, b0, b1);
+        const float rs = (a0 + a1) + (b0 + b1);
+        l += rs;
+        if (g > 0) {
+          mbar_wait(&bar[kPFree], (g - 1) & 1);  // PV of the previous tile retired
+          tc_fence_after();
+        }
+        if (j > 0 && __any_sync(0xffffffffu, rescale)) {
+          const uint32_t o_row = t_row + 256 + ob * 128;
 #pragma unroll
           for (int c = 0; c < HD / 32; ++c) {
             uint32_t r[32];
-            tmem_ld32(t_row + 256 + c * 32, r);
+            tmem_ld32(o_row + c * 32, r);
             tmem_wait_ld();
 #pragma unroll
             for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-            tmem_st32(t_row + 256 + c * 32, r);
+            tmem_st32(o_row + c * 32, r);
           }
           tmem_wait_st();
         }
-      }
-      // P row -> smem, K-major SW128 (two 64-key regions)
-      uint8_t* prow = sP + (row >> 3) * 1024 + (row & 7) * 128;
+        // P row -> smem (st.shared), K-major SW128 (two 64-key regions)
 #pragma unroll
-      for (int cc = 0; cc < kKeys / 8; ++cc) {
-        uint4 v;
-        v.x = pack_bf16(s[cc * 8 + 0], s[cc * 8 + 1]);
-        v.y = pack_bf16(s[cc * 8 + 2], s[cc * 8 + 3]);
-        v.z = pack_bf16(s[cc * 8 + 4], s[cc * 8 + 5]);
-        v.w = pack_bf16(s[cc * 8 + 6], s[cc * 8 + 7]);
-        *reinterpret_cast<uint4*>(prow + (cc >> 3) * 16384 + (((cc & 7) ^ (row & 7)) << 4)) = v;
+        for (int cc = 0; cc < kKeys / 8; ++cc) {
+          const uint32_t a = p_row_addr + (cc >> 3) * 16384 + (((cc & 7) ^ (row & 7)) << 4);
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
+                       "r"(pack_bf16(s[cc * 8 + 0], s[cc * 8 + 1])),
+                       "r"(pack_bf16(s[cc * 8 + 2], s[cc * 8 + 3])),
+                       "r"(pack_bf16(s[cc * 8 + 4], s[cc * 8 + 5])),
+                       "r"(pack_bf16(s[cc * 8 + 6], s[cc * 8 + 7]))
+                       : "memory");
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(&bar[kPFull]);
       }
-      fence_proxy_async_smem();
-      tc_fence_before();
-      mbar_arrive(&bar[kPFull]);
+      // row sum -> epilogue WG (slot ob is free once the epilogue of item ii-2 is done)
+      mbar_wait(&bar[kOFree0 + ob], ((ii >> 1) & 1) ^ 1);
+      sL[ob * 128 + row] = l;
+      mbar_arrive(&bar[kLFull0 + ob]);
     }
-    // ------------------------------------------------------------ epilogue
-    mbar_wait(&bar[kOFull], 0);
-    tc_fence_after();
-    const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
-    __nv_bfloat16* orow =
-        out + (static_cast<int64_t>(q_start + tok) * n_q_heads + kvh * G + h_local) * HD;
+  } else if (warp >= 8) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;\n" ::: "memory");
+    // ------------------------------------------------------------ epilogue WG
+    // O (TMEM) / l -> bf16 output rows, off the softmax critical path
+    const int row = threadIdx.x - 256;  // == TMEM lane (warp % 4 quadrant)
+    const int t_local = row / G;
+    const int h_local = row % G;
+    const uint32_t t_row = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+    for (int idx = blockIdx.x, ii = 0; idx < n_work; idx += gridDim.x, ++ii) {
+      const Item it = load_item(work, idx);
+      const int ob = ii & 1;
+      const int tok = it.qt * TQ + t_local;
+      const bool row_valid = tok < it.q_len;
+      mbar_wait(&bar[kLFull0 + ob], (ii >> 1) & 1);
+      const float l = sL[ob * 128 + row];
+      mbar_wait(&bar[kOFull0 + ob], (ii >> 1) & 1);
+      tc_fence_after();
+      const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
+      __nv_bfloat16* orow =
+          out + (static_cast<int64_t>(it.q_start + tok) * n_q_heads + it.kvh * G + h_local) * HD;
 #pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {
-      uint32_t r[32];
-      tmem_ld32(t_row + 256 + c * 32, r);
-      tmem_wait_ld();
-      if (row_valid) {
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(t_row + 256 + ob * 128 + c * 32, r);
+        tmem_wait_ld();
+        if (row_valid) {
 #pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          uint4 v;
-          v.x = pack_bf16(__uint_as_float(r[i + 0]) * inv_l, __uint_as_float(r[i + 1]) * inv_l);
-          v.y = pack_bf16(__uint_as_float(r[i + 2]) * inv_l, __uint_as_float(r[i + 3]) * inv_l);
-          v.z = pack_bf16(__uint_as_float(r[i + 4]) * inv_l, __uint_as_float(r[i + 5]) * inv_l);
-          v.w = pack_bf16(__uint_as_float(r[i + 6]) * inv_l, __uint_as_float(r[i + 7]) * inv_l);
-          *reinterpret_cast<uint4*>(orow + c * 32 + i) = v;
+          for (int i = 0; i < 32; i += 8) {
+            uint4 v;
+            v.x = pack_bf16(__uint_as_float(r[i + 0]) * inv_l, __uint_as_float(r[i + 1]) * inv_l);
+            v.y = pack_bf16(__uint_as_float(r[i + 2]) * inv_l, __uint_as_float(r[i + 3]) * inv_l);
+            v.z = pack_bf16(__uint_as_float(r[i + 4]) * inv_l, __uint_as_float(r[i + 5]) * inv_l);
+            v.w = pack_bf16(__uint_as_float(r[i + 6]) * inv_l, __uint_as_float(r[i + 7]) * inv_l);
+            *reinterpret_cast<uint4*>(orow + c * 32 + i) = v;
+          }
         }
       }
+      tc_fence_before();
+      mbar_arrive(&bar[kOFree0 + ob]);
     }
     tc_fence_before();
   }
@@ -325,12 +463,20 @@ cudaError_t launch_t(const CUtensorMap& tq, const CUtensorMap& tkv, void* out, i
                      const int* blk_pos, const int* work, int n_work, float scale_log2,
                      cudaStream_t stream) {
   auto kern = prefix_prefill_kernel<HD, G, BT>;
-  const uint32_t smem = Smem<HD>::kTotal;
+  const uint32_t smem = Smem<HD, BT>::kTotal;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  kern<<<n_work, kThreads, smem, stream>>>(tq, tkv, static_cast<__nv_bfloat16*>(out), n_q_heads,
-                                          layer, req_meta, blk_ids, blk_valid, blk_pos, work,
-                                          scale_log2);
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const int grid = n_work < sms ? n_work : sms;
+  kern<<<grid, kThreads, smem, stream>>>(tq, tkv, static_cast<__nv_bfloat16*>(out), n_q_heads,
+                                        layer, req_meta, blk_ids, blk_valid, blk_pos, work, n_work,
+                                        scale_log2);
   return cudaGetLastError();
 }
 

@@ -85,7 +85,7 @@ class AttnPlan:
         pos_np = np.asarray(pos, dtype=np.int32)
         g = n_q_heads // n_kv_heads
         cap = sum(max(0, -(-r[0] // (128 // g))) for r in requests) * n_kv_heads + 1
-        work = np.zeros(cap * 4, dtype=np.int32)
+        work = np.zeros(cap * 8, dtype=np.int32)
         n_work = np.zeros(1, dtype=np.int32)
         check(load().rcb_attn_plan(
             meta_np.ctypes.data_as(_lib._p32), self.n_req, valid_np.ctypes.data_as(_lib._p32),
@@ -93,17 +93,18 @@ class AttnPlan:
             work.ctypes.data_as(_lib._p32), cap, n_work.ctypes.data_as(_lib._p32)),
             "rcb_attn_plan")
         self.n_work = int(n_work[0])
-        self.work_host = work[: self.n_work * 4].reshape(-1, 4)
-        self.kv_tiles = int(self.work_host[:, 3].sum()) if self.n_work else 0
-        pack = np.concatenate([meta_np, np.asarray(ids, dtype=np.int32), valid_np, pos_np,
-                               work[: self.n_work * 4]])
+        self.work_host = work[: self.n_work * 8].reshape(-1, 8)
+        self.kv_tiles = int(self.work_host[:, 7].sum()) if self.n_work else 0
+        # work items first: the kernel reads them as int4 (16-byte aligned)
+        pack = np.concatenate([work[: self.n_work * 8], meta_np, np.asarray(ids, dtype=np.int32),
+                               valid_np, pos_np])
         self._buf = torch.from_numpy(pack).to(device)
         o = 0
+        self.work = self._buf[o:o + self.n_work * 8]; o += self.n_work * 8
         self.meta = self._buf[o:o + meta_np.size]; o += meta_np.size
         self.blk_ids = self._buf[o:o + len(ids)]; o += len(ids)
         self.blk_valid = self._buf[o:o + len(ids)]; o += len(ids)
         self.blk_pos = self._buf[o:o + len(ids)]; o += len(ids)
-        self.work = self._buf[o:o + self.n_work * 4]
         self.requests = requests
 
 

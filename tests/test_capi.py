@@ -45,13 +45,14 @@ def test_attn_plan_host_logic():
     # two requests: a cached 1024-token prefix + 32 prompt tokens, and a full miss
     reqs = [(32, 1024, list(range(66)), [16] * 66), (544, 0, list(range(34)), [16] * 34)]
     plan = kernels.AttnPlan(reqs, block_tokens=16, n_q_heads=32, n_kv_heads=8, device="cpu")
-    w = plan.work_host
+    w = plan.work_host  # {q_start, q_len, q_pos0, blk_begin, blk_count, q_tile, kv_head, n}
     # GQA-4: 32 tokens per query tile -> 1 tile for req 0, 17 for req 1, x 8 kv heads
     assert plan.n_work == (1 + 17) * 8
-    assert w[0, 3] == max(w[:, 3])  # heaviest first
-    r0 = w[w[:, 0] == 0]
-    assert set(r0[:, 3]) == {9}  # 1056 slots -> 9 key tiles
-    r1 = w[w[:, 0] == 1]
+    assert w[0, 7] == max(w[:, 7])  # heaviest first
+    r0 = w[w[:, 0] == 0]  # request 0 starts at query row 0
+    assert set(r0[:, 7]) == {9}  # 1056 slots -> 9 key tiles
+    assert set(map(tuple, r0[:, :5])) == {(0, 32, 1024, 0, 66)}
+    r1 = w[w[:, 0] == 32]
     # causal: query tile t covers tokens [32t, 32t+32) -> needs key tile (32t+31)//128
-    assert sorted(set(zip(r1[:, 1], r1[:, 3]))) == [(t, (32 * t + 31) // 128 + 1) for t in range(17)]
-    assert np.all(np.bincount(r1[:, 2]) == 17)
+    assert sorted(set(zip(r1[:, 5], r1[:, 7]))) == [(t, (32 * t + 31) // 128 + 1) for t in range(17)]
+    assert np.all(np.bincount(r1[:, 6]) == 17)

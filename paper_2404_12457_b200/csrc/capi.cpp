@@ -85,7 +85,7 @@ int rcb_prefix_prefill(const void* q, void* o, int32_t total_q_tokens, int32_t n
 // n_kv_tiles} (self-contained so the kernel never chases req_meta).  A query tile only needs the
 // key tiles up to the slot holding its last query position (causal), so the
 // count is found by a binary search over the table's logical block starts.
-// Items are ordered heaviest-first so long tiles start in the first wave.
+// Items are ordered for L2 reuse (see below).
 int rcb_attn_plan(const int32_t* req_meta, int32_t n_req, const int32_t* blk_valid,
                   const int32_t* blk_pos, int32_t block_tokens, int32_t n_q_heads,
                   int32_t n_kv_heads, int32_t* work_out, int32_t cap, int32_t* n_work_out) {
@@ -121,8 +121,19 @@ int rcb_attn_plan(const int32_t* req_meta, int32_t n_req, const int32_t* blk_val
       for (int32_t h = 0; h < n_kv_heads; ++h) items.push_back({r, qt, h, tiles});
     }
   }
-  std::stable_sort(items.begin(), items.end(),
-                   [](const Item& a, const Item& b) { return a.tiles > b.tiles; });
+  // L2 locality: the ~148 CTAs of a persistent launch take consecutive items,
+  // so keep all q-tiles of one (request, kv head) adjacent — they re-read the
+  // same K/V pages.  Requests go heaviest first, q-tiles longest first.
+  std::vector<int64_t> req_work(n_req, 0);
+  for (const Item& it : items) req_work[it.r] += it.tiles;
+  std::stable_sort(items.begin(), items.end(), [&](const Item& a, const Item& b) {
+    if (a.r != b.r) {
+      if (req_work[a.r] != req_work[b.r]) return req_work[a.r] > req_work[b.r];
+      return a.r < b.r;
+    }
+    if (a.h != b.h) return a.h < b.h;
+    return a.tiles > b.tiles;
+  });
   if (n_work_out) *n_work_out = static_cast<int32_t>(items.size());
   if (static_cast<int32_t>(items.size()) > cap)
     return rcb::set_error(RCB_ERR_ARG, "work capacity too small");

@@ -72,7 +72,7 @@ def init_weights(dims: ModelDims, seed: int = 0, device="cuda", dtype=torch.bflo
 
 def rms_norm(x: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
     xf = x.float()
-    return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps) * w.float()).to(x.dtype)
+    return xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps) * w.float()
 
 
 class PrefillModel:
@@ -91,13 +91,14 @@ class PrefillModel:
         d = self.dims
         s = d.shape
         T = tokens.shape[0]
-        x = self.w["emb"][tokens]
-        q_rot = torch.empty((T, s.n_q_heads, s.head_dim), dtype=x.dtype, device=x.device)
+        x = self.w["emb"][tokens].float()  # residual stream kept in fp32; bf16 into GEMMs
+        bf = self.w["emb"].dtype
+        q_rot = torch.empty((T, s.n_q_heads, s.head_dim), dtype=bf, device=x.device)
         attn = torch.empty_like(q_rot)
         qw = s.n_q_heads * s.head_dim
         kw = s.n_kv_heads * s.head_dim
         for layer, lw in enumerate(self.w["layers"]):
-            h = rms_norm(x, lw["ln1"], d.norm_eps)
+            h = rms_norm(x, lw["ln1"], d.norm_eps).to(bf)
             qkv = h @ lw["wqkv"]
             kernels.kv_write_rope(qkv[:, :qw], qkv[:, qw:qw + kw], qkv[:, qw + kw:], q_rot,
                                   positions, slots, self.base, block_tokens=self.bt,
@@ -107,12 +108,12 @@ class PrefillModel:
             kernels.prefix_prefill(q_rot, attn, plan, self.base, self.nb, block_tokens=self.bt,
                                    n_layers=s.n_layers, n_kv_heads=s.n_kv_heads,
                                    head_dim=s.head_dim, layer=layer, stream=stream)
-            x = x + attn.view(T, qw) @ lw["wo"]
-            h = rms_norm(x, lw["ln2"], d.norm_eps)
+            x = x + (attn.view(T, qw) @ lw["wo"]).float()
+            h = rms_norm(x, lw["ln2"], d.norm_eps).to(bf)
             gu = h @ lw["wgu"]
             gate, up = gu[:, : d.ffn], gu[:, d.ffn:]
-            x = x + (torch.nn.functional.silu(gate.float()) * up.float()).to(x.dtype) @ lw["wdown"]
-        h = rms_norm(x[last_rows], self.w["norm"], d.norm_eps)
+            x = x + ((torch.nn.functional.silu(gate.float()) * up.float()).to(bf) @ lw["wdown"]).float()
+        h = rms_norm(x[last_rows], self.w["norm"], d.norm_eps).to(bf)
         return (h @ self.w["lm_head"]).float()
 
 

@@ -74,6 +74,5 @@ def test_cached_prefix_prefill_matches_full_recompute():
     err_b, _ = run([1, 2], [], prompts[1])
     err_c, _ = run([1], [3], prompts[2])
     assert mag > 0.1  # logits are not trivially small
-    assert err_a <= LOGIT_ATOL, err_a
-    assert err_b <= LOGIT_ATOL, err_b
-    assert err_c <= LOGIT_ATOL, err_c
+    errs = (err_a, err_b, err_c)
+    assert max(errs) <= LOGIT_ATOL, f"max |logit err| per request {errs} (max |logit| {mag:.3f})"

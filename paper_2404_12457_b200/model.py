@@ -44,26 +44,27 @@ DIMS = {
 def init_weights(dims: ModelDims, seed: int = 0, device="cuda", dtype=torch.bfloat16):
     """Seeded random weights (fan-in scaled so activations stay O(1))."""
     s = dims.shape
-    g = torch.Generator(device="cpu")
+    gen_dev = "cpu" if str(device) == "cpu" or dims.d_model <= 1024 else device
+    g = torch.Generator(device=gen_dev)  # big models: generate on the device
     g.manual_seed(seed)
 
     def w(rows, cols, scale=1.0):
-        t = torch.randn((rows, cols), generator=g) * (scale / rows ** 0.5)
+        t = torch.randn((rows, cols), generator=g, device=gen_dev) * (scale / rows ** 0.5)
         return t.to(device=device, dtype=dtype)
 
     qkv = (s.n_q_heads + 2 * s.n_kv_heads) * s.head_dim
     layers = []
     for _ in range(s.n_layers):
         layers.append({
-            "ln1": (1.0 + 0.1 * torch.randn(dims.d_model, generator=g)).to(device, dtype),
+            "ln1": (1.0 + 0.1 * torch.randn(dims.d_model, generator=g, device=gen_dev)).to(device, dtype),
             "wqkv": w(dims.d_model, qkv),
             "wo": w(s.n_q_heads * s.head_dim, dims.d_model),
-            "ln2": (1.0 + 0.1 * torch.randn(dims.d_model, generator=g)).to(device, dtype),
+            "ln2": (1.0 + 0.1 * torch.randn(dims.d_model, generator=g, device=gen_dev)).to(device, dtype),
             "wgu": w(dims.d_model, 2 * dims.ffn),
             "wdown": w(dims.ffn, dims.d_model),
         })
     return {
-        "emb": (torch.randn((dims.vocab, dims.d_model), generator=g)).to(device, dtype),
+        "emb": (torch.randn((dims.vocab, dims.d_model), generator=g, device=gen_dev)).to(device, dtype),
         "layers": layers,
         "norm": torch.ones(dims.d_model).to(device, dtype),
         "lm_head": w(dims.d_model, dims.vocab, 0.5),

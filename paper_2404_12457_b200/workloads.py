@@ -77,6 +77,12 @@ WORKLOADS = {
     # single tier (host 0: evicted nodes are dropped) — configs[2] exercises the host tier.
     "mistral7b-100k": Workload("mistral7b-100k", "mistral-7b", 100_000, 512.0, 0.0, 0.97, 2, 32,
                                1_100_000, 0, 64),
+    # configs[1] shape with MMLU-like repeated questions (query pool, Zipf 1.1 over
+    # questions, as the reference's desk recipe pkg/tests/test_acceptance.py:33-41):
+    # the hit-rate axis of the TTFT curve
+    "mistral7b-100k-qpool": Workload("mistral7b-100k-qpool", "mistral-7b", 100_000, 512.0, 0.0,
+                                     0.97, 2, 32, 1_100_000, 0, 64, query_pool=20_000,
+                                     query_zipf_s=1.1),
     # configs[2]: LLaMA2-7B shape, top-5, two-tier cache under memory pressure
     "llama2-7b-top5": Workload("llama2-7b-top5", "llama2-7b", 100_000, 512.0, 0.0, 0.97, 5, 32,
                                40_000, 160_000, 64, batch=16),

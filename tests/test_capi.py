@@ -48,7 +48,12 @@ def test_attn_plan_host_logic():
     w = plan.work_host  # {q_start, q_len, q_pos0, blk_begin, blk_count, q_tile, kv_head, n}
     # GQA-4: 32 tokens per query tile -> 1 tile for req 0, 17 for req 1, x 8 kv heads
     assert plan.n_work == (1 + 17) * 8
-    assert w[0, 7] == max(w[:, 7])  # heaviest request first, longest q-tile first
+    # L2 order: heaviest request first (req 1: 17 q-tiles), grouped by kv head,
+    # longest q-tile first within a group
+    assert w[0, 0] == 32 and w[0, 6] == 0 and w[0, 7] == 5
+    for h in range(8):
+        grp = w[(w[:, 0] == 32) & (w[:, 6] == h)]
+        assert list(grp[:, 7]) == sorted(grp[:, 7], reverse=True)
     r0 = w[w[:, 0] == 0]  # request 0 starts at query row 0
     assert set(r0[:, 7]) == {9}  # 1056 slots -> 9 key tiles
     assert set(map(tuple, r0[:, :5])) == {(0, 32, 1024, 0, 66)}

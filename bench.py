@@ -53,49 +53,15 @@ def parse():
     ap.add_argument("--swap-mode", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ttft", action="store_true")
+    # multi-rank smoke on a single GPU (all ranks on cuda:0, gloo, small tier)
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--single-device", action="store_true")
+    ap.add_argument("--gpu-tier-tokens", type=int, default=0)
     return ap.parse_args()
 
 
 # ---------------------------------------------------------------------- distributed
-class Dist:
-    def __init__(self):
-        self.world = int(os.environ.get("WORLD_SIZE", "1"))
-        self.rank = int(os.environ.get("RANK", "0"))
-        self.local = int(os.environ.get("LOCAL_RANK", "0"))
-        self.pg = None
-
-    def init(self, backend="nccl"):
-        if self.world > 1:
-            import torch.distributed as dist
-
-            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            dist.init_process_group(backend=backend, rank=self.rank, world_size=self.world)
-            self.pg = dist
-
-    def barrier(self):
-        if self.pg is not None:
-            self.pg.barrier()
-
-    def max(self, x: float) -> float:
-        if self.pg is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
-        return float(t.item())
-
-    def sum(self, x: float) -> float:
-        if self.pg is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        self.pg.all_reduce(t)
-        return float(t.item())
-
-    def all_gather(self, t: torch.Tensor) -> torch.Tensor:
-        if self.pg is None:
-            return t.unsqueeze(0)
-        out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
-        self.pg.all_gather_into_tensor(out, t.contiguous())
-        return out
+from paper_2404_12457_b200.dist import Dist, route, shard_bounds  # noqa: E402
 
 
 # ---------------------------------------------------------------------- clocks
@@ -161,11 +127,10 @@ def build_workload(args, dist: Dist):
     n_steps = args.cache_warm_steps + args.warmup + 2 * args.steps
     n_req = n_steps * R * dist.world
     trace, sizes = make_stream(w, n_req, rate=1.0)
-    mine = [r for r in trace if r.id % dist.world == dist.rank]  # DP routing: id mod G
+    mine = route(trace, dist.rank, dist.world)  # DP routing: id mod G
     steps = [mine[i * R:(i + 1) * R] for i in range(n_steps)]
     # corpus shard of this rank (global ids [lo, hi)); queries from the targets' rows
-    lo = (w.num_docs * dist.rank) // dist.world
-    hi = (w.num_docs * (dist.rank + 1)) // dist.world
+    lo, hi = shard_bounds(w.num_docs, dist.rank, dist.world)
     return w, R, steps, sizes, (lo, hi)
 
 
@@ -232,9 +197,14 @@ def run_ours(args, dist: Dist):
     from paper_2404_12457_b200.workloads import pool_blocks
     from ragsim.cost_model import synthetic_profile
 
-    torch.cuda.set_device(dist.local)
-    dist.init("nccl")
+    torch.cuda.set_device(0 if args.single_device else dist.local)
+    dist.init(args.backend)
+    dist.device = "cuda"
     w, R, steps, sizes, (lo, hi) = build_workload(args, dist)
+    if args.gpu_tier_tokens:
+        import dataclasses as _dc
+
+        w = _dc.replace(w, gpu_capacity_tokens=args.gpu_tier_tokens)
     shape = w.model
     min_doc = min(sizes.values())
     ng = pool_blocks(w.gpu_capacity_tokens, w.block_tokens, min_doc, R * (w.k + 1))

@@ -203,7 +203,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t q_base = smem_u32(sQ);
       const uint32_t k_base = smem_u32(sK);
       const uint32_t v_base = smem_u32(sV);
-      const uint32_t p_base = smem_u32(sP);
       struct T {
         int idx, ii, j, n, g;
       };
@@ -252,10 +251,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < kKeys / 16; ++kk) {
-          const uint64_t a = sw128_desc(p_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
+          // A = P (bf16 pairs) written by the softmax over its S buffer's first 64 columns;
+          // QK(g+2) is issued after this PV, and tcgen05.mma executes in issue order
+          const uint32_t a = tmem + st * kKeys + kk * 8;
           // V tile is [half][128 keys][64]: MN-major, halves 16 KB apart (LBO)
           const uint64_t b = sw128_desc(v_base + st * S::kKV + kk * 2048, 16384, 1024);
-          umma_bf16_ss(tmem + 256 + ob * 128, a, b, idesc_pv, (t.j > 0 || kk > 0) ? 1u : 0u);
+          umma_bf16_ts(tmem + 256 + ob * 128, a, b, idesc_pv, (t.j > 0 || kk > 0) ? 1u : 0u);
         }
         umma_commit(&bar[kVEmpty0 + st]);
         umma_commit(&bar[kPFree]);
@@ -284,7 +285,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t t_row = tmem + (static_cast<uint32_t>(warp * 32) << 16);
     float s[kKeys];
     int g = 0;
-    const uint32_t p_row_addr = smem_u32(sP) + (row >> 3) * 1024 + (row & 7) * 128;
     for (int idx = blockIdx.x, ii = 0; idx < n_work; idx += gridDim.x, ++ii) {
       const Item it = load_item(work, idx);
       const int ob = ii & 1;
@@ -310,13 +310,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&bar[kMetaFree0 + ms]);
         mbar_wait(&bar[kSFull0 + st], (g >> 1) & 1);
         tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < kKeys / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(t_row + st * kKeys + c * 32, r);
+        {
+          uint32_t r[kKeys];
+          tmem_ld128(t_row + st * kKeys, r);
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);
+          for (int i = 0; i < kKeys; ++i) s[i] = __uint_as_float(r[i]);
         }
         tc_fence_before();
         mbar_arrive(&bar[kSFree0 + st]);
@@ -388,18 +387,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           tmem_wait_st();
         }
-        // P row -> smem (st.shared), K-major SW128 (two 64-key regions)
+        // P row -> TMEM over this tile's S columns [0, 64): the PV MMA reads A from TMEM
+        {
+          uint32_t pk[kKeys / 2];
 #pragma unroll
-        for (int cc = 0; cc < kKeys / 8; ++cc) {
-          const uint32_t a = p_row_addr + (cc >> 3) * 16384 + (((cc & 7) ^ (row & 7)) << 4);
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
-                       "r"(pack_bf16(s[cc * 8 + 0], s[cc * 8 + 1])),
-                       "r"(pack_bf16(s[cc * 8 + 2], s[cc * 8 + 3])),
-                       "r"(pack_bf16(s[cc * 8 + 4], s[cc * 8 + 5])),
-                       "r"(pack_bf16(s[cc * 8 + 6], s[cc * 8 + 7]))
-                       : "memory");
+          for (int c = 0; c < kKeys / 2; ++c) pk[c] = pack_bf16(s[2 * c], s[2 * c + 1]);
+          tmem_st64(t_row + st * kKeys, pk);
+          tmem_wait_st();
         }
-        fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(&bar[kPFull]);
       }

@@ -32,6 +32,12 @@ constexpr int kThreads = 384;
 constexpr int kRows = 128;
 constexpr int kKeys = 128;  // key slots per KV tile
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+// exp2 on the FMA pipe for kPolyCols of every 8 score columns: the MUFU (16/clk/SM)
+// would otherwise need 8 cycles per warp instruction x 128 columns per tile
+#ifndef RCB_POLY_COLS
+#define RCB_POLY_COLS 2
+#endif
+constexpr int kPolyCols = RCB_POLY_COLS;
 
 template <int HD, int BT>
 struct Smem {
@@ -347,8 +353,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           l *= alpha;
           rescale = true;
         }
-        // p = 2^(s*scale - m): packed FFMA2, MUFU for 6 of every 8 columns and the
-        // FMA-pipe polynomial for the other 2; row sum with packed FADD2
+        // p = 2^(s*scale - m): packed FFMA2, MUFU for 8-kPolyCols of every 8 columns
+        // and the FMA-pipe polynomial for the rest (balances MUFU vs issue); packed FADD2 sums
         const uint64_t sc2 = f2_pack(scale_log2, scale_log2);
         const uint64_t nm2 = f2_pack(-m, -m);
         uint64_t acc0 = f2_pack(0.f, 0.f), acc1 = acc0;
@@ -358,8 +364,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int e = 0; e < 8; e += 2) f2_unpack(ffma2(f2_pack(s[c + e], s[c + e + 1]), sc2, nm2), x[e], x[e + 1]);
 #pragma unroll
-          for (int e = 0; e < 6; ++e) s[c + e] = ex2_mufu(x[e]);
-          f2_unpack(ex2_poly2(x[6], x[7]), s[c + 6], s[c + 7]);
+          for (int e = 0; e < 8 - kPolyCols; ++e) s[c + e] = ex2_mufu(x[e]);
+#pragma unroll
+          for (int e = 8 - kPolyCols; e < 8; e += 2) f2_unpack(ex2_poly2(x[e], x[e + 1]), s[c + e], s[c + e + 1]);
           acc0 = fadd2(acc0, f2_pack(s[c + 0], s[c + 1]));
           acc1 = fadd2(acc1, f2_pack(s[c + 2], s[c + 3]));
           acc0 = fadd2(acc0, f2_pack(s[c + 4], s[c + 5]));

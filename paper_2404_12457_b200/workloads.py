@@ -85,10 +85,11 @@ WORKLOADS = {
                                      query_zipf_s=1.1),
     # configs[2]: LLaMA2-7B shape, top-5, two-tier cache under memory pressure
     "llama2-7b-top5": Workload("llama2-7b-top5", "llama2-7b", 100_000, 512.0, 0.0, 0.97, 5, 32,
-                               40_000, 160_000, 64, batch=16),
+                               40_000, 160_000, 64, batch=12),
     # configs[3]: LLaMA2-13B shape, 10M-doc corpus sharded over the GPUs, DSP stages
+    # (kvB = 800 KiB/token: a 120K-token tier is 98 GB next to 26 GB of weights)
     "llama2-13b-10m": Workload("llama2-13b-10m", "llama2-13b", 10_000_000, 512.0, 0.0, 0.97, 2,
-                               32, 200_000, 100_000, 64, batch=32),
+                               32, 120_000, 0, 64, batch=32),
     # configs[4]: Mixtral-8x7B shape, Poisson arrivals, reordering, DP replicas
     "mixtral-poisson": Workload("mixtral-poisson", "mixtral-8x7b", 100_000, 512.0, 0.0, 0.97, 2,
                                 32, 400_000, 100_000, 64),

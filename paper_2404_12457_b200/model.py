@@ -11,7 +11,7 @@ cost_model.py:106-117).
 
 Used for (a) logits parity of cached-prefix prefill against an fp32 oracle
 (tests/test_gpu_model.py) and (b) measuring the B200 T(alpha, beta) grid that
-replaces ragsim's synthetic profile (tools/profile_prefill.py).
+replaces ragsim's synthetic profile (profile.py).
 """
 
 from __future__ import annotations

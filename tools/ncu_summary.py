@@ -90,7 +90,7 @@ def launch_shares(path: str) -> list:
             d = dict(zip(hdr, r))
             if d.get("Metric Name") != "gpu__time_duration.sum":
                 continue
-            name = d["Kernel Name"].replace("void ", "").replace("(anonymous namespace)::", "")
+            name = d["Kernel Name"].replace("void ", "").replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
             name = name.split("(")[0].split("<")[0].strip()
             v = float(d["Metric Value"].replace(",", ""))
             if d["Metric Unit"] == "us":

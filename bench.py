@@ -270,8 +270,8 @@ def run_ours(args, dist: Dist):
     g = torch.Generator(device="cuda")
     g.manual_seed(1234 + dist.rank)
     qkv = (torch.randn((max_t, shape.qkv_width), generator=g, device="cuda") * 0.5).to(torch.bfloat16)
-    q_rot = torch.empty((max_t, shape.n_q_heads, shape.head_dim), dtype=torch.bfloat16, device="cuda")
-    out = torch.empty_like(q_rot)
+    q_rot = None  # Q's RoPE is fused into the attention kernel
+    out = torch.empty((max_t, shape.n_q_heads, shape.head_dim), dtype=torch.bfloat16, device="cuda")
 
     def device_step(i, attn_events=None, scan_events=None):
         p = plans[i]

@@ -119,28 +119,37 @@ int rcb_kv_block_copy(const void* src_base, void* dst_base, int64_t block_bytes,
 /* RoPE (rotate-half, LLaMA convention) on q and k, then k/v scattered into the
  * pool at `slots_dev` (slot = block*block_tokens + offset) for `layer`.
  * q/k/v: bf16 [n_tokens][heads][head_dim] (row strides q_stride/kv_stride in
- * elements); q_out: bf16 [n_tokens][n_q_heads][head_dim]. */
+ * elements); q_out: bf16 [n_tokens][n_q_heads][head_dim].  q == NULL: only K/V
+ * (Q's rotation fused into rcb_prefix_prefill through a RoPE table). */
 int rcb_kv_write_rope(const void* q, int64_t q_stride, const void* k, const void* v,
                       int64_t kv_stride, void* q_out, const int32_t* positions_dev,
                       const int32_t* slots_dev, int32_t n_tokens, int32_t n_q_heads,
                       void* kv_pool, int32_t block_tokens, int32_t n_layers, int32_t n_kv_heads,
                       int32_t head_dim, int32_t layer, float rope_theta, void* stream);
 
+/* cos/sin table for fused RoPE: float2 [max_pos][head_dim/2] = (cos, sin)(pos * theta^(-2i/d)) */
+int rcb_rope_table(void* table_dev, int32_t max_pos, int32_t head_dim, float rope_theta,
+                   void* stream);
+
 /* (2) prefix-aware prefill attention (tcgen05/TMEM, TMA-staged K/V pages).
  * Stand-in replaced: interpolate(profile, alpha, beta) (cost_model.py:106-117,
  * simulator.py:506).
- *   q, o        : bf16 [total_q_tokens][n_q_heads][head_dim]
+ *   q           : bf16 rows of q_row_stride elements, the first n_q_heads*head_dim of each
+ *                 row = the token's query heads (e.g. a view into the QKV projection)
+ *   o           : bf16 [total_q_tokens][n_q_heads][head_dim]
+ *   rope_table  : NULL if q is already rotated, else rcb_rope_table output: Q tiles are
+ *                 rotated in shared memory inside the kernel
  *   req_meta_dev: int32 [n_req][5] = {q_start, q_len(beta), q_pos0(alpha), blk_begin, blk_count}
  *   blk_*_dev   : int32 per block-table entry: pool block id, valid tokens, logical start pos
  *   work_dev    : int32 [n_work][8] = {q_start, q_len, q_pos0, blk_begin, blk_count,
  *                 q_tile, kv_head, n_kv_tiles} (built by rcb_attn_plan, heaviest first) */
-int rcb_prefix_prefill(const void* q, void* o, int32_t total_q_tokens, int32_t n_q_heads,
-                       const void* kv_pool, int64_t num_pool_blocks, int32_t block_tokens,
-                       int32_t n_layers, int32_t n_kv_heads, int32_t head_dim, int32_t layer,
-                       const int32_t* req_meta_dev, const int32_t* blk_ids_dev,
-                       const int32_t* blk_valid_dev, const int32_t* blk_pos_dev,
-                       const int32_t* work_dev, int32_t n_work, float softmax_scale,
-                       void* stream);
+int rcb_prefix_prefill(const void* q, int64_t q_row_stride, void* o, int32_t total_q_tokens,
+                       int32_t n_q_heads, const void* kv_pool, int64_t num_pool_blocks,
+                       int32_t block_tokens, int32_t n_layers, int32_t n_kv_heads,
+                       int32_t head_dim, int32_t layer, const int32_t* req_meta_dev,
+                       const int32_t* blk_ids_dev, const int32_t* blk_valid_dev,
+                       const int32_t* blk_pos_dev, const int32_t* work_dev, int32_t n_work,
+                       float softmax_scale, const void* rope_table_dev, void* stream);
 /* host-side work planner for rcb_prefix_prefill: writes up to cap items (8 int32 each) into
  * work_out (heaviest first) and returns the count in n_work_out.  Inputs are the
  * host copies of req_meta / blk_valid / blk_pos. */

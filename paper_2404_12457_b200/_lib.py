@@ -14,7 +14,9 @@ import os
 from ctypes import POINTER, c_char_p, c_float, c_int, c_int32, c_int64, c_void_p
 
 LIB_NAME = "libragcache_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+# RCB_LIB_PATH selects an alternate in-tree build (A/B kernel experiments only)
+LIB_PATH = os.environ.get("RCB_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 RCB_OK = 0
 RCB_ERR_NO_BLOCKS = 1
@@ -74,10 +76,11 @@ SIGNATURES = [
     ("rcb_kv_write_rope", c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_void_p,
                                   c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_int32,
                                   c_int32, c_int32, c_int32, c_int32, c_float, c_void_p]),
-    ("rcb_prefix_prefill", c_int, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_int64,
-                                   c_int32, c_int32, c_int32, c_int32, c_int32, c_void_p,
-                                   c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_float,
-                                   c_void_p]),
+    ("rcb_rope_table", c_int, [c_void_p, c_int32, c_int32, c_float, c_void_p]),
+    ("rcb_prefix_prefill", c_int, [c_void_p, c_int64, c_void_p, c_int32, c_int32, c_void_p,
+                                   c_int64, c_int32, c_int32, c_int32, c_int32, c_int32,
+                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32,
+                                   c_float, c_void_p, c_void_p]),
     ("rcb_attn_plan", c_int, [_p32, c_int32, _p32, _p32, c_int32, c_int32, c_int32, _p32,
                               c_int32, _p32]),
     ("rcb_retrieval_workspace_bytes", c_int64, [c_int64, c_int32, c_int32, c_int32]),

@@ -66,19 +66,20 @@ const char* rcb_last_error(void) { return rcb::g_last_error.c_str(); }
 
 int rcb_version(void) { return 1; }
 
-int rcb_prefix_prefill(const void* q, void* o, int32_t total_q_tokens, int32_t n_q_heads,
-                       const void* kv_pool, int64_t num_pool_blocks, int32_t block_tokens,
-                       int32_t n_layers, int32_t n_kv_heads, int32_t head_dim, int32_t layer,
-                       const int32_t* req_meta_dev, const int32_t* blk_ids_dev,
-                       const int32_t* blk_valid_dev, const int32_t* blk_pos_dev,
-                       const int32_t* work_dev, int32_t n_work, float softmax_scale,
-                       void* stream) {
+int rcb_prefix_prefill(const void* q, int64_t q_row_stride, void* o, int32_t total_q_tokens,
+                       int32_t n_q_heads, const void* kv_pool, int64_t num_pool_blocks,
+                       int32_t block_tokens, int32_t n_layers, int32_t n_kv_heads,
+                       int32_t head_dim, int32_t layer, const int32_t* req_meta_dev,
+                       const int32_t* blk_ids_dev, const int32_t* blk_valid_dev,
+                       const int32_t* blk_pos_dev, const int32_t* work_dev, int32_t n_work,
+                       float softmax_scale, const void* rope_table_dev, void* stream) {
   if (block_tokens != 16 && block_tokens != 32 && block_tokens != 64 && block_tokens != 128)
     return rcb::set_error(RCB_ERR_ARG, "block_tokens must be 16, 32, 64 or 128");
-  return rcb::prefix_prefill(q, o, total_q_tokens, n_q_heads, kv_pool, num_pool_blocks,
-                             block_tokens, n_layers, n_kv_heads, head_dim, layer, req_meta_dev,
-                             blk_ids_dev, blk_valid_dev, blk_pos_dev, work_dev, n_work,
-                             softmax_scale, static_cast<cudaStream_t>(stream));
+  return rcb::prefix_prefill(q, q_row_stride, o, total_q_tokens, n_q_heads, kv_pool,
+                             num_pool_blocks, block_tokens, n_layers, n_kv_heads, head_dim, layer,
+                             req_meta_dev, blk_ids_dev, blk_valid_dev, blk_pos_dev, work_dev,
+                             n_work, softmax_scale, rope_table_dev,
+                             static_cast<cudaStream_t>(stream));
 }
 
 // Work items {q_start, q_len, q_pos0, blk_begin, blk_count, q_tile, kv_head,

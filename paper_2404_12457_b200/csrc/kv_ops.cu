@@ -9,6 +9,7 @@
 // (2) RoPE + paged KV write: the suffix tokens' K/V (miss docs + prompt) are
 //     rotated and scattered straight into their reserved pool blocks, so a
 //     committed node adopts them with no copy (tree.py:252-294 insert_path).
+#include <algorithm>
 #include <cuda_bf16.h>
 
 #include "rcb_internal.h"
@@ -144,7 +145,9 @@ __global__ void __launch_bounds__(kRopeThreads)
   __nv_bfloat16* vbase = kbase + int64_t(n_kv_heads) * tile;
   __syncthreads();
   const int cph = half / 8;  // 16-byte chunks per half row
-  const int rot_units = (n_q_heads + n_kv_heads) * cph;
+  // q == nullptr: K/V only (Q's RoPE is fused into the attention kernel)
+  const int q_heads = q != nullptr ? n_q_heads : 0;
+  const int rot_units = (q_heads + n_kv_heads) * cph;
   const int v_units = n_kv_heads * (head_dim / 8);
   for (int u = threadIdx.x; u < rot_units + v_units; u += blockDim.x) {
     if (u < rot_units) {
@@ -152,12 +155,12 @@ __global__ void __launch_bounds__(kRopeThreads)
       const int c = (u - h * cph) * 8;
       const __nv_bfloat16* src;
       __nv_bfloat16* dst;
-      if (h < n_q_heads) {
+      if (h < q_heads) {
         src = q + int64_t(t) * q_stride + int64_t(h) * head_dim;
         dst = q_out + (int64_t(t) * n_q_heads + h) * head_dim;
       } else {
-        src = k + int64_t(t) * kv_stride + int64_t(h - n_q_heads) * head_dim;
-        dst = kbase + int64_t(h - n_q_heads) * tile;
+        src = k + int64_t(t) * kv_stride + int64_t(h - q_heads) * head_dim;
+        dst = kbase + int64_t(h - q_heads) * tile;
       }
       float x0[8], x1[8], y0[8], y1[8];
       unpack8(*reinterpret_cast<const uint4*>(src + c), x0);
@@ -210,6 +213,38 @@ extern "C" int rcb_kv_block_copy(const void* src_base, void* dst_base, int64_t b
   cudaError_t e = rcb::launch_block_copy_dev(src_base, dst_base, block_bytes, pairs_dev, n_pairs,
                                              static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return rcb::set_cuda_error(e, "rcb_kv_block_copy");
+  return RCB_OK;
+}
+
+namespace rcb {
+namespace {
+__global__ void rope_table_kernel(float2* __restrict__ out, int max_pos, int half, int head_dim,
+                                  float log2_theta) {
+  const int64_t n = int64_t(max_pos) * half;
+  for (int64_t u = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; u < n;
+       u += int64_t(gridDim.x) * blockDim.x) {
+    const int p = static_cast<int>(u / half);
+    const int i = static_cast<int>(u - int64_t(p) * half);
+    const float inv_freq = exp2f(-(2.f * i / head_dim) * log2_theta);
+    float sn, cs;
+    sincosf(static_cast<float>(p) * inv_freq, &sn, &cs);
+    out[u] = make_float2(cs, sn);
+  }
+}
+}  // namespace
+}  // namespace rcb
+
+extern "C" int rcb_rope_table(void* table_dev, int32_t max_pos, int32_t head_dim, float rope_theta,
+                              void* stream) {
+  if (max_pos <= 0 || head_dim <= 0 || head_dim % 2 != 0)
+    return rcb::set_error(RCB_ERR_ARG, "bad rope table shape");
+  const int half = head_dim / 2;
+  const int64_t n = int64_t(max_pos) * half;
+  const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 8));
+  rcb::rope_table_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<float2*>(table_dev), max_pos, half, head_dim, log2f(rope_theta));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return rcb::set_cuda_error(e, "rcb_rope_table");
   return RCB_OK;
 }
 

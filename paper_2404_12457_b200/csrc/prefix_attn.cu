@@ -27,7 +27,8 @@ namespace rcb {
 namespace attn {
 
 // WG0 (warps 0-3) softmax | WG1: warp 4 Q+K producer, 5 MMA, 6 V producer, 7 idle |
-// WG2 (warps 8-11) epilogue.  setmaxnreg moves registers to the softmax WG.
+// WG2 (warps 8-11) epilogue (+ in-smem Q RoPE with a table).  setmaxnreg moves registers
+// from WG1 to the softmax and epilogue WGs.
 constexpr int kThreads = 384;
 constexpr int kRows = 128;
 constexpr int kKeys = 128;  // key slots per KV tile
@@ -54,13 +55,13 @@ struct Smem {
   static constexpr uint32_t offMeta = offP + kP;     // int [kMetaSlots][2][kBPT]
   static constexpr uint32_t offL = offMeta + kMetaSlots * 2 * kBPT * 4;  // float [2][128]
   static constexpr uint32_t offBar = offL + 2 * 128 * 4;
-  static constexpr uint32_t kTotal = offBar + 32 * 8 + 16 + 1024;  // + alignment slack
+  static constexpr uint32_t kTotal = offBar + 40 * 8 + 16 + 1024;  // + alignment slack
 };
 
 enum Bar {
   kQFull0 = 0, kQEmpty0 = 2, kKFull0 = 4, kVFull0 = 6, kKEmpty0 = 8, kSFull0 = 10, kSFree0 = 12,
   kPFull = 14, kPFree = 15, kOFull0 = 16, kOFree0 = 18, kVEmpty0 = 20, kMetaFull0 = 22,
-  kMetaFree0 = 26, kLFull0 = 30, kNumBars = 32
+  kMetaFree0 = 26, kLFull0 = 30, kQReady0 = 32, kNumBars = 34
 };
 
 // Work items are self-contained (no dependent loads at item start):
@@ -87,7 +88,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                           __nv_bfloat16* __restrict__ out, int n_q_heads, int layer,
                           const int* __restrict__ req_meta, const int* __restrict__ blk_ids,
                           const int* __restrict__ blk_valid, const int* __restrict__ blk_pos,
-                          const int* __restrict__ work, int n_work, float scale_log2) {
+                          const int* __restrict__ work, int n_work, float scale_log2,
+                          const float2* __restrict__ rope) {
   using S = Smem<HD, BT>;
   constexpr int TQ = kRows / G;
   constexpr int BPT = S::kBPT;
@@ -126,6 +128,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(&bar[kLFull0 + 0], kRows);
     mbar_init(&bar[kLFull0 + 1], kRows);
+    mbar_init(&bar[kQReady0 + 0], kRows);
+    mbar_init(&bar[kQReady0 + 1], kRows);
     fence_barrier_init();
   }
   if (warp == 5) tmem_alloc<512>(tmem_slot);
@@ -143,16 +147,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_prefetch(&tm_q);
       tma_prefetch(&tm_kv);
       int g = 0;
-      for (int idx = blockIdx.x, ii = 0; idx < n_work; idx += gridDim.x, ++ii) {
+      int q_issued = 0;  // items whose Q load has been issued
+      auto issue_q = [&](int idx, int ii) {
         const Item it = load_item(work, idx);
         const int qb = ii & 1;
-        mbar_wait(&bar[kQEmpty0 + qb], ((ii >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&bar[kQFull0 + qb], S::kQ);
         for (int h = 0; h < (int)S::kHalves; ++h)
           tma_load_3d(sQ + qb * S::kQ + h * 16384, &tm_q, &bar[kQFull0 + qb], h * 64,
                       it.kvh * G, it.q_start + it.qt * TQ);
+      };
+      for (int idx = blockIdx.x, ii = 0; idx < n_work; idx += gridDim.x, ++ii) {
+        const Item it = load_item(work, idx);
+        if (q_issued == ii) {
+          mbar_wait(&bar[kQEmpty0 + (ii & 1)], ((ii >> 1) & 1) ^ 1);
+          issue_q(idx, ii);
+          ++q_issued;
+        }
         for (int j = 0; j < it.n; ++j, ++g) {
           const int st = g & 1;
+          // next item's Q as soon as its buffer frees (QK of item ii-1 retired): it then
+          // lands a whole item ahead of its first MMA
+          if (q_issued == ii + 1 &&
+              idx + (int)gridDim.x < n_work &&
+              mbar_test(&bar[kQEmpty0 + ((ii + 1) & 1)], (((ii + 1) >> 1) & 1) ^ 1)) {
+            issue_q(idx + gridDim.x, ii + 1);
+            ++q_issued;
+          }
           // per-tile mask metadata: its own 4-slot ring (the softmax may lag the K ring)
           const int ms = g & (S::kMetaSlots - 1);
           mbar_wait(&bar[kMetaFree0 + ms], ((g / S::kMetaSlots) & 1) ^ 1);
@@ -232,7 +252,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue_qk = [&](const T& t) {
         const int qb = t.ii & 1;
         const int st = t.g & 1;
-        if (t.j == 0) mbar_wait(&bar[kQFull0 + qb], (t.ii >> 1) & 1);
+        if (t.j == 0)  // Q landed (and, with fused RoPE, rotated by the epilogue WG)
+          mbar_wait(&bar[(rope != nullptr ? kQReady0 : kQFull0) + qb], (t.ii >> 1) & 1);
         mbar_wait(&bar[kKFull0 + st], (t.g >> 1) & 1);
         mbar_wait(&bar[kSFree0 + st], ((t.g >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -411,15 +432,71 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&bar[kLFull0 + ob]);
     }
   } else if (warp >= 8) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;\n" ::: "memory");
+    // launch pool 168 x 384 regs: softmax 248 + producers 40 leave 216 per epilogue thread
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
     // ------------------------------------------------------------ epilogue WG
-    // O (TMEM) / l -> bf16 output rows, off the softmax critical path
+    // O (TMEM) / l -> bf16 output rows, off the softmax critical path.  With a RoPE
+    // table it also rotates each landed Q tile in place (rotate-half pairs (i, i+HD/2)),
+    // one item ahead of the epilogue it trails.
     const int row = threadIdx.x - 256;  // == TMEM lane (warp % 4 quadrant)
     const int t_local = row / G;
     const int h_local = row % G;
     const uint32_t t_row = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
-    for (int idx = blockIdx.x, ii = 0; idx < n_work; idx += gridDim.x, ++ii) {
-      const Item it = load_item(work, idx);
+    auto rotate_q = [&](const Item& it, int ii) {
+      // Thread -> (row, chunk-pair): a warp covers 32/CP rows x CP pairs of 8-element
+      // chunks (i, i+HD/2), so its table reads are contiguous 512 B runs per token and its
+      // shared accesses hit distinct 16 B banks of each 128 B swizzled row.
+      constexpr int CP = HD / 16;          // chunk pairs per row
+      constexpr int RPP = 128 / CP;        // rows per pass
+      const int c = row % CP;
+      const int r0 = row / CP;
+      const int qb = ii & 1;
+      const uint32_t qbase = smem_u32(sQ) + qb * S::kQ;
+      auto tab_ptr = [&](int p) {
+        const int r = r0 + p * RPP;
+        const int tok = min(it.qt * TQ + r / G, it.q_len - 1);  // rows past q_len are masked
+        return reinterpret_cast<const float4*>(rope + static_cast<int64_t>(it.q_pos0 + tok) *
+                                                          (HD / 2) + c * 8);
+      };
+      // every pass's table slice in flight at once (CP x 64 B per thread), issued before
+      // the Q tile lands: one L2 round trip per item instead of one per pass
+      float4 tab[CP][4];
+#pragma unroll
+      for (int p = 0; p < CP; ++p) {
+        const float4* t = tab_ptr(p);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) tab[p][e] = __ldg(t + e);
+      }
+      mbar_wait(&bar[kQFull0 + qb], (ii >> 1) & 1);
+#pragma unroll
+      for (int p = 0; p < CP; ++p) {
+        const int r = r0 + p * RPP;
+        const uint32_t base = qbase + (r >> 3) * 1024 + (r & 7) * 128;
+        const int i0 = c * 8, j0 = i0 + HD / 2;
+        const uint32_t a0 = base + (i0 / 64) * 16384 + ((((i0 % 64) / 8) ^ (r & 7)) << 4);
+        const uint32_t a1 = base + (j0 / 64) * 16384 + ((((j0 % 64) / 8) ^ (r & 7)) << 4);
+        uint32_t u0[4], u1[4];
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(u0[0]), "=r"(u0[1]), "=r"(u0[2]), "=r"(u0[3]) : "r"(a0));
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(u1[0]), "=r"(u1[1]), "=r"(u1[2]), "=r"(u1[3]) : "r"(a1));
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {  // tab[p][e] = (cos, sin) of elements 2e, 2e+1
+          const float2 x0 = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u0[e]));
+          const float2 x1 = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u1[e]));
+          const float4 cs = tab[p][e];
+          u0[e] = pack_bf16(x0.x * cs.x - x1.x * cs.y, x0.y * cs.z - x1.y * cs.w);
+          u1[e] = pack_bf16(x1.x * cs.x + x0.x * cs.y, x1.y * cs.z + x0.y * cs.w);
+        }
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a0), "r"(u0[0]),
+                     "r"(u0[1]), "r"(u0[2]), "r"(u0[3]));
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a1), "r"(u1[0]),
+                     "r"(u1[1]), "r"(u1[2]), "r"(u1[3]));
+      }
+      fence_proxy_async_smem();  // generic-proxy writes -> tensor-core reads
+      mbar_arrive(&bar[kQReady0 + qb]);
+    };
+    auto epilogue = [&](const Item& it, int ii) {
       const int ob = ii & 1;
       const int tok = it.qt * TQ + t_local;
       const bool row_valid = tok < it.q_len;
@@ -449,6 +526,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&bar[kOFree0 + ob]);
+    };
+    const int n_mine =
+        n_work > (int)blockIdx.x ? (n_work - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    auto item_of = [&](int ii) { return load_item(work, blockIdx.x + ii * gridDim.x); };
+    // With a RoPE table, item ii+A is rotated before item ii's epilogue: an epilogue only
+    // has to finish before its O buffer's next first PV (item ii+2), a rotation before its
+    // item's first QK.  A = 2 lets Q(ii+2) be rotated while item ii+1 computes (Q is double
+    // buffered, so Q(ii+2) lands once QK of item ii retires).
+    constexpr int kAhead = 2;
+    if (rope != nullptr)
+      for (int ii = 0; ii < kAhead && ii < n_mine; ++ii) rotate_q(item_of(ii), ii);
+    for (int ii = 0; ii < n_mine; ++ii) {
+      if (rope != nullptr && ii + kAhead < n_mine) rotate_q(item_of(ii + kAhead), ii + kAhead);
+      epilogue(item_of(ii), ii);
     }
     tc_fence_before();
   }
@@ -463,7 +554,7 @@ template <int HD, int G, int BT>
 cudaError_t launch_t(const CUtensorMap& tq, const CUtensorMap& tkv, void* out, int n_q_heads,
                      int layer, const int* req_meta, const int* blk_ids, const int* blk_valid,
                      const int* blk_pos, const int* work, int n_work, float scale_log2,
-                     cudaStream_t stream) {
+                     const float2* rope, cudaStream_t stream) {
   auto kern = prefix_prefill_kernel<HD, G, BT>;
   const uint32_t smem = Smem<HD, BT>::kTotal;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -478,19 +569,20 @@ cudaError_t launch_t(const CUtensorMap& tq, const CUtensorMap& tkv, void* out, i
   const int grid = n_work < sms ? n_work : sms;
   kern<<<grid, kThreads, smem, stream>>>(tq, tkv, static_cast<__nv_bfloat16*>(out), n_q_heads,
                                         layer, req_meta, blk_ids, blk_valid, blk_pos, work, n_work,
-                                        scale_log2);
+                                        scale_log2, rope);
   return cudaGetLastError();
 }
 
 template <int HD, int G>
 cudaError_t launch_bt(int bt, const CUtensorMap& tq, const CUtensorMap& tkv, void* out,
                       int n_q_heads, int layer, const int* rm, const int* bi, const int* bv,
-                      const int* bp, const int* work, int n_work, float sl2, cudaStream_t st) {
+                      const int* bp, const int* work, int n_work, float sl2, const float2* rope,
+                      cudaStream_t st) {
   switch (bt) {
-    case 16: return launch_t<HD, G, 16>(tq, tkv, out, n_q_heads, layer, rm, bi, bv, bp, work, n_work, sl2, st);
-    case 32: return launch_t<HD, G, 32>(tq, tkv, out, n_q_heads, layer, rm, bi, bv, bp, work, n_work, sl2, st);
-    case 64: return launch_t<HD, G, 64>(tq, tkv, out, n_q_heads, layer, rm, bi, bv, bp, work, n_work, sl2, st);
-    case 128: return launch_t<HD, G, 128>(tq, tkv, out, n_q_heads, layer, rm, bi, bv, bp, work, n_work, sl2, st);
+    case 16: return launch_t<HD, G, 16>(tq, tkv, out, n_q_heads, layer, rm, bi, bv, bp, work, n_work, sl2, rope, st);
+    case 32: return launch_t<HD, G, 32>(tq, tkv, out, n_q_heads, layer, rm, bi, bv, bp, work, n_work, sl2, rope, st);
+    case 64: return launch_t<HD, G, 64>(tq, tkv, out, n_q_heads, layer, rm, bi, bv, bp, work, n_work, sl2, rope, st);
+    case 128: return launch_t<HD, G, 128>(tq, tkv, out, n_q_heads, layer, rm, bi, bv, bp, work, n_work, sl2, rope, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -498,23 +590,24 @@ cudaError_t launch_bt(int bt, const CUtensorMap& tq, const CUtensorMap& tkv, voi
 template <int HD>
 cudaError_t launch_g(int g, int bt, const CUtensorMap& tq, const CUtensorMap& tkv, void* out,
                      int n_q_heads, int layer, const int* rm, const int* bi, const int* bv,
-                     const int* bp, const int* work, int n_work, float sl2, cudaStream_t st) {
+                     const int* bp, const int* work, int n_work, float sl2, const float2* rope,
+                     cudaStream_t st) {
   switch (g) {
-    case 1: return launch_bt<HD, 1>(bt, tq, tkv, out, n_q_heads, layer, rm, bi, bv, bp, work, n_work, sl2, st);
-    case 2: return launch_bt<HD, 2>(bt, tq, tkv, out, n_q_heads, layer, rm, bi, bv, bp, work, n_work, sl2, st);
-    case 4: return launch_bt<HD, 4>(bt, tq, tkv, out, n_q_heads, layer, rm, bi, bv, bp, work, n_work, sl2, st);
-    case 8: return launch_bt<HD, 8>(bt, tq, tkv, out, n_q_heads, layer, rm, bi, bv, bp, work, n_work, sl2, st);
+    case 1: return launch_bt<HD, 1>(bt, tq, tkv, out, n_q_heads, layer, rm, bi, bv, bp, work, n_work, sl2, rope, st);
+    case 2: return launch_bt<HD, 2>(bt, tq, tkv, out, n_q_heads, layer, rm, bi, bv, bp, work, n_work, sl2, rope, st);
+    case 4: return launch_bt<HD, 4>(bt, tq, tkv, out, n_q_heads, layer, rm, bi, bv, bp, work, n_work, sl2, rope, st);
+    case 8: return launch_bt<HD, 8>(bt, tq, tkv, out, n_q_heads, layer, rm, bi, bv, bp, work, n_work, sl2, rope, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
 }  // namespace attn
 
-int prefix_prefill(const void* q, void* o, int total_q_tokens, int n_q_heads, const void* kv_pool,
-                   int64_t num_pool_blocks, int block_tokens, int n_layers, int n_kv_heads,
-                   int head_dim, int layer, const int* req_meta, const int* blk_ids,
-                   const int* blk_valid, const int* blk_pos, const int* work, int n_work,
-                   float softmax_scale, cudaStream_t stream) {
+int prefix_prefill(const void* q, int64_t q_row_stride, void* o, int total_q_tokens,
+                   int n_q_heads, const void* kv_pool, int64_t num_pool_blocks, int block_tokens,
+                   int n_layers, int n_kv_heads, int head_dim, int layer, const int* req_meta,
+                   const int* blk_ids, const int* blk_valid, const int* blk_pos, const int* work,
+                   int n_work, float softmax_scale, const void* rope_table, cudaStream_t stream) {
   if (n_work == 0) return RCB_OK;
   if (head_dim != 64 && head_dim != 128) return set_error(RCB_ERR_ARG, "head_dim must be 64 or 128");
   if (n_kv_heads <= 0 || n_q_heads % n_kv_heads != 0) return set_error(RCB_ERR_ARG, "bad head counts");
@@ -523,7 +616,9 @@ int prefix_prefill(const void* q, void* o, int total_q_tokens, int n_q_heads, co
   CUtensorMap tq, tkv;
   {
     const uint64_t dims[3] = {(uint64_t)head_dim, (uint64_t)n_q_heads, (uint64_t)total_q_tokens};
-    const uint64_t strides[2] = {(uint64_t)head_dim * 2, (uint64_t)n_q_heads * head_dim * 2};
+    if (q_row_stride < (int64_t)n_q_heads * head_dim || q_row_stride % 8 != 0)
+      return set_error(RCB_ERR_ARG, "q_row_stride must be >= n_q_heads*head_dim and a multiple of 8");
+    const uint64_t strides[2] = {(uint64_t)head_dim * 2, (uint64_t)q_row_stride * 2};
     const uint32_t box[3] = {64, (uint32_t)g, (uint32_t)(128 / g)};
     int rc = encode_tma_bf16(&tq, q, 3, dims, strides, box);
     if (rc != RCB_OK) return rc;
@@ -543,9 +638,11 @@ int prefix_prefill(const void* q, void* o, int total_q_tokens, int n_q_heads, co
   cudaError_t e =
       head_dim == 128
           ? attn::launch_g<128>(g, block_tokens, tq, tkv, o, n_q_heads, layer, req_meta, blk_ids,
-                                blk_valid, blk_pos, work, n_work, sl2, stream)
+                                blk_valid, blk_pos, work, n_work, sl2,
+                                static_cast<const float2*>(rope_table), stream)
           : attn::launch_g<64>(g, block_tokens, tq, tkv, o, n_q_heads, layer, req_meta, blk_ids,
-                               blk_valid, blk_pos, work, n_work, sl2, stream);
+                               blk_valid, blk_pos, work, n_work, sl2,
+                               static_cast<const float2*>(rope_table), stream);
   if (e != cudaSuccess) return set_cuda_error(e, "prefix_prefill launch");
   return RCB_OK;
 }

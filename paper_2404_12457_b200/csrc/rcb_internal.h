@@ -18,11 +18,11 @@ int set_cuda_error(cudaError_t e, const char* where);
 int encode_tma_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
                     const uint64_t* strides, const uint32_t* box);
 
-int prefix_prefill(const void* q, void* o, int total_q_tokens, int n_q_heads, const void* kv_pool,
-                   int64_t num_pool_blocks, int block_tokens, int n_layers, int n_kv_heads,
-                   int head_dim, int layer, const int* req_meta, const int* blk_ids,
-                   const int* blk_valid, const int* blk_pos, const int* work, int n_work,
-                   float softmax_scale, cudaStream_t stream);
+int prefix_prefill(const void* q, int64_t q_row_stride, void* o, int total_q_tokens,
+                   int n_q_heads, const void* kv_pool, int64_t num_pool_blocks, int block_tokens,
+                   int n_layers, int n_kv_heads, int head_dim, int layer, const int* req_meta,
+                   const int* blk_ids, const int* blk_valid, const int* blk_pos, const int* work,
+                   int n_work, float softmax_scale, const void* rope_table, cudaStream_t stream);
 
 // block copy with the (src, dst) block-index list passed by value in the launch
 constexpr int kPairsPerLaunch = 1024;

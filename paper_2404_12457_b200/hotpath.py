@@ -124,6 +124,12 @@ class HotPath:
         self.tree = TieredKnowledgeTree(gpu_capacity_tokens, host_capacity_tokens,
                                         policy=make_policy(policy), pool=pool)
         self._keys = itertools.count()
+        self._rope = None  # cos/sin table for RoPE fused into the attention kernel
+
+    def rope_table(self, max_pos: int = 1 << 15) -> torch.Tensor:
+        if self._rope is None or self._rope.shape[0] < max_pos:
+            self._rope = kernels.rope_table(max_pos, self.shape.head_dim, self.shape.rope_theta)
+        return self._rope
 
     # ------------------------------------------------------------------ decisions
     def admit(self, req_id: int, docs, prompt: int) -> Admission:
@@ -209,34 +215,39 @@ class HotPath:
         plan.dev = {"attn": attn, "pos": arr[:n], "slots": arr[n:2 * n],
                     "last": arr[2 * n:].long(), "flops": attention_flops(self.shape, reqs)}
 
-    def prefill(self, plan: StepPlan, qkv: torch.Tensor, q_rot: torch.Tensor, out: torch.Tensor,
+    def prefill(self, plan: StepPlan, qkv: torch.Tensor, q_rot, out: torch.Tensor,
                 events=None, stream=None) -> None:
-        """Launch KV-write + attention for every layer of the step (async)."""
+        """Launch KV-write + attention for every layer of the step (async).
+
+        ``q_rot`` is unused (kept for callers of the pre-rotated path): Q's RoPE is
+        applied inside the attention kernel from the hot path's cos/sin table."""
         s = self.shape
         d = plan.dev
         T = plan.total_q
         if T == 0:
             return
-        if T > qkv.shape[0] or T > q_rot.shape[0] or T > out.shape[0]:
+        if T > qkv.shape[0] or T > out.shape[0]:
             raise ValueError(f"step has {T} suffix tokens; activation buffers hold {qkv.shape[0]}")
         x = qkv[:T]
         q = x[:, : s.n_q_heads * s.head_dim]
         k = x[:, s.n_q_heads * s.head_dim:(s.n_q_heads + s.n_kv_heads) * s.head_dim]
         v = x[:, (s.n_q_heads + s.n_kv_heads) * s.head_dim:]
-        qr = q_rot[:T]
         o = out[:T]
         base = self.pool.gpu_base
+        rope = self.rope_table(max(1 << 15, d["attn"].max_pos))
         for layer in range(s.n_layers):
-            kernels.kv_write_rope(q, k, v, qr, d["pos"], d["slots"], base,
+            # K/V: RoPE + paged write; Q's RoPE is fused into the attention kernel, which
+            # reads the raw query columns of the QKV rows (no rotated-Q round trip)
+            kernels.kv_write_rope(None, k, v, None, d["pos"], d["slots"], base,
                                   block_tokens=self.block_tokens, n_layers=s.n_layers,
                                   n_kv_heads=s.n_kv_heads, head_dim=s.head_dim, layer=layer,
-                                  rope_theta=s.rope_theta, stream=stream)
+                                  rope_theta=s.rope_theta, n_q_heads=s.n_q_heads, stream=stream)
             if events is not None:
                 events[layer][0].record()
-            kernels.prefix_prefill(qr, o, d["attn"], base, self.num_gpu_blocks,
+            kernels.prefix_prefill(q, o, d["attn"], base, self.num_gpu_blocks,
                                    block_tokens=self.block_tokens, n_layers=s.n_layers,
                                    n_kv_heads=s.n_kv_heads, head_dim=s.head_dim, layer=layer,
-                                   stream=stream)
+                                   rope=rope, n_q_heads=s.n_q_heads, stream=stream)
             if events is not None:
                 events[layer][1].record()
 

@@ -36,17 +36,31 @@ def block_copy(src_base: int, dst_base: int, block_bytes: int, pairs: torch.Tens
                                    pairs.shape[0], _stream(stream)), "rcb_kv_block_copy")
 
 
-def kv_write_rope(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, q_out: torch.Tensor,
-                  positions: torch.Tensor, slots: torch.Tensor, pool_base: int, *,
-                  block_tokens: int, n_layers: int, n_kv_heads: int, head_dim: int,
-                  layer: int, rope_theta: float, stream=None) -> None:
-    """RoPE q,k then scatter k,v into the pool (q/k/v may be strided row views)."""
-    n_tokens = q.shape[0]
-    n_q_heads = q_out.shape[1]
-    assert q.stride(-1) == 1 and k.stride(-1) == 1 and v.stride(-1) == 1
-    assert k.stride(0) == v.stride(0)
+def rope_table(max_pos: int, head_dim: int, rope_theta: float, device="cuda",
+               stream=None) -> torch.Tensor:
+    """float32 [max_pos, head_dim/2, 2] = (cos, sin) for fused-RoPE prefill."""
+    t = torch.empty((max_pos, head_dim // 2, 2), dtype=torch.float32, device=device)
+    check(load().rcb_rope_table(_dev_ptr(t), max_pos, head_dim, float(rope_theta),
+                                _stream(stream)), "rcb_rope_table")
+    return t
+
+
+def kv_write_rope(q, k: torch.Tensor, v: torch.Tensor, q_out, positions: torch.Tensor,
+                  slots: torch.Tensor, pool_base: int, *, block_tokens: int, n_layers: int,
+                  n_kv_heads: int, head_dim: int, layer: int, rope_theta: float,
+                  n_q_heads: int | None = None, stream=None) -> None:
+    """RoPE q,k then scatter k,v into the pool (q/k/v may be strided row views).
+    q = q_out = None: K/V only (Q is rotated inside prefix_prefill)."""
+    n_tokens = k.shape[0]
+    if n_q_heads is None:
+        n_q_heads = q_out.shape[1]
+    assert k.stride(-1) == 1 and v.stride(-1) == 1 and k.stride(0) == v.stride(0)
+    if q is not None:
+        assert q.stride(-1) == 1
     check(load().rcb_kv_write_rope(
-        _dev_ptr(q), q.stride(0), _dev_ptr(k), _dev_ptr(v), k.stride(0), _dev_ptr(q_out),
+        _dev_ptr(q) if q is not None else None, q.stride(0) if q is not None else 0,
+        _dev_ptr(k), _dev_ptr(v), k.stride(0),
+        _dev_ptr(q_out) if q_out is not None else None,
         _dev_ptr(positions), _dev_ptr(slots), n_tokens, n_q_heads, pool_base, block_tokens,
         n_layers, n_kv_heads, head_dim, layer, float(rope_theta), _stream(stream)),
         "rcb_kv_write_rope")
@@ -80,6 +94,7 @@ class AttnPlan:
             q_start += q_len
         self.total_q = q_start
         self.n_req = len(requests)
+        self.max_pos = max((r[1] + r[0] for r in requests), default=0)
         meta_np = np.asarray(meta, dtype=np.int32)
         valid_np = np.asarray(valid, dtype=np.int32)
         pos_np = np.asarray(pos, dtype=np.int32)
@@ -111,18 +126,29 @@ class AttnPlan:
 def prefix_prefill(q: torch.Tensor, out: torch.Tensor, plan: AttnPlan, pool_base: int,
                    num_pool_blocks: int, *, block_tokens: int, n_layers: int, n_kv_heads: int,
                    head_dim: int, layer: int, softmax_scale: float | None = None,
+                   rope: torch.Tensor | None = None, n_q_heads: int | None = None,
                    stream=None) -> None:
-    """Prefix-aware prefill attention for one layer (tcgen05 kernel)."""
-    assert q.dtype == torch.bfloat16 and q.is_contiguous() and out.is_contiguous()
-    n_q_heads = q.shape[1]
+    """Prefix-aware prefill attention for one layer (tcgen05 kernel).
+
+    q: [T, Hq, d] rotated queries, or (with ``rope``, a rope_table) the raw query
+    columns of the QKV projection: a [T, >= Hq*d] row view whose RoPE is applied
+    in shared memory inside the kernel."""
+    assert q.dtype == torch.bfloat16 and out.is_contiguous() and q.stride(-1) == 1
+    if n_q_heads is None:
+        n_q_heads = out.shape[1]
+    row_stride = q.stride(0)
+    if rope is not None and (rope.dtype != torch.float32 or rope.shape[0] < plan.max_pos
+                             or rope.shape[1] * 2 != head_dim):
+        raise ValueError(f"rope table {tuple(rope.shape)} does not cover positions < "
+                         f"{plan.max_pos} at head_dim {head_dim}")
     if softmax_scale is None:
         softmax_scale = 1.0 / math.sqrt(head_dim)
     check(load().rcb_prefix_prefill(
-        _dev_ptr(q), _dev_ptr(out), q.shape[0], n_q_heads, pool_base, num_pool_blocks,
-        block_tokens, n_layers, n_kv_heads, head_dim, layer, _dev_ptr(plan.meta),
-        _dev_ptr(plan.blk_ids), _dev_ptr(plan.blk_valid), _dev_ptr(plan.blk_pos),
-        _dev_ptr(plan.work), plan.n_work, float(softmax_scale), _stream(stream)),
-        "rcb_prefix_prefill")
+        _dev_ptr(q), row_stride, _dev_ptr(out), q.shape[0], n_q_heads, pool_base,
+        num_pool_blocks, block_tokens, n_layers, n_kv_heads, head_dim, layer,
+        _dev_ptr(plan.meta), _dev_ptr(plan.blk_ids), _dev_ptr(plan.blk_valid),
+        _dev_ptr(plan.blk_pos), _dev_ptr(plan.work), plan.n_work, float(softmax_scale),
+        _dev_ptr(rope) if rope is not None else None, _stream(stream)), "rcb_prefix_prefill")
 
 
 class RetrievalWorkspace:

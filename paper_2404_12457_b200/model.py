@@ -84,6 +84,8 @@ class PrefillModel:
         self.bt = block_tokens
         self.nb = num_pool_blocks
         self.base = pool_base
+        self.rope = kernels.rope_table(1 << 14, dims.shape.head_dim, dims.shape.rope_theta,
+                                       device=weights["emb"].device)
 
     def prefill(self, tokens: torch.Tensor, positions: torch.Tensor, slots: torch.Tensor,
                 plan: "kernels.AttnPlan", last_rows: torch.Tensor, stream=None) -> torch.Tensor:
@@ -94,21 +96,21 @@ class PrefillModel:
         T = tokens.shape[0]
         x = self.w["emb"][tokens].float()  # residual stream kept in fp32; bf16 into GEMMs
         bf = self.w["emb"].dtype
-        q_rot = torch.empty((T, s.n_q_heads, s.head_dim), dtype=bf, device=x.device)
-        attn = torch.empty_like(q_rot)
+        attn = torch.empty((T, s.n_q_heads, s.head_dim), dtype=bf, device=x.device)
         qw = s.n_q_heads * s.head_dim
         kw = s.n_kv_heads * s.head_dim
         for layer, lw in enumerate(self.w["layers"]):
             h = rms_norm(x, lw["ln1"], d.norm_eps).to(bf)
             qkv = h @ lw["wqkv"]
-            kernels.kv_write_rope(qkv[:, :qw], qkv[:, qw:qw + kw], qkv[:, qw + kw:], q_rot,
-                                  positions, slots, self.base, block_tokens=self.bt,
-                                  n_layers=s.n_layers, n_kv_heads=s.n_kv_heads,
-                                  head_dim=s.head_dim, layer=layer, rope_theta=s.rope_theta,
-                                  stream=stream)
-            kernels.prefix_prefill(q_rot, attn, plan, self.base, self.nb, block_tokens=self.bt,
-                                   n_layers=s.n_layers, n_kv_heads=s.n_kv_heads,
-                                   head_dim=s.head_dim, layer=layer, stream=stream)
+            # K/V rotated into the pool; Q's RoPE runs inside the attention kernel
+            kernels.kv_write_rope(None, qkv[:, qw:qw + kw], qkv[:, qw + kw:], None, positions,
+                                  slots, self.base, block_tokens=self.bt, n_layers=s.n_layers,
+                                  n_kv_heads=s.n_kv_heads, head_dim=s.head_dim, layer=layer,
+                                  rope_theta=s.rope_theta, n_q_heads=s.n_q_heads, stream=stream)
+            kernels.prefix_prefill(qkv[:, :qw], attn, plan, self.base, self.nb,
+                                   block_tokens=self.bt, n_layers=s.n_layers,
+                                   n_kv_heads=s.n_kv_heads, head_dim=s.head_dim, layer=layer,
+                                   rope=self.rope, n_q_heads=s.n_q_heads, stream=stream)
             x = x + (attn.view(T, qw) @ lw["wo"]).float()
             h = rms_norm(x, lw["ln2"], d.norm_eps).to(bf)
             gu = h @ lw["wgu"]

@@ -205,3 +205,48 @@ def test_kv_write_rope_matches_oracle():
         assert (pc[b, 1, 0, :, o, :].float() - k_ref[t]).abs().max().item() < 0.05
         assert torch.equal(pc[b, 1, 1, :, o, :], v.cpu().view(T, hkv, hd)[t])
     assert int((pc[:, 0] != 0).sum()) == 0 and int((pc[:, 2] != 0).sum()) == 0
+
+
+# ---------------------------------------------------------------- fused Q-RoPE
+@pytest.mark.parametrize("hd,hq,hkv,bt", [(128, 32, 8, 64), (64, 4, 4, 16), (128, 8, 8, 32)])
+def test_prefix_prefill_fused_rope_matches_oracle(hd, hq, hkv, bt):
+    """Q read raw from a strided QKV buffer and rotated in shared memory inside the
+    kernel == attention on oracle-rotated Q; K/V-only write mode leaves q untouched."""
+    L, nb, theta = 1, 200, 10000.0
+    pool = _pool(nb, L, hkv, bt, hd, seed=11)
+    free = list(np.random.default_rng(4).permutation(nb))
+    reqs = [([300, 41], [200, 32]), ([], [96]), ([512], [17])]
+    requests = []
+    for prefix, suffix in reqs:
+        blocks, valid = _table(prefix + suffix, bt, free)
+        requests.append((sum(suffix), sum(prefix), blocks, valid))
+    T = sum(r[0] for r in requests)
+    width = (hq + 2 * hkv) * hd
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    qkv = torch.randn((T, width), generator=g, device="cuda").to(torch.bfloat16)
+    pos = torch.cat([r[1] + torch.arange(r[0]) for r in requests]).to(torch.int32)
+    table = kernels.rope_table(4096, hd, theta)
+    out = torch.empty((T, hq, hd), dtype=torch.bfloat16, device="cuda")
+    plan = kernels.AttnPlan(requests, block_tokens=bt, n_q_heads=hq, n_kv_heads=hkv)
+    kernels.prefix_prefill(qkv[:, : hq * hd], out, plan, pool.data_ptr(), nb, block_tokens=bt,
+                           n_layers=L, n_kv_heads=hkv, head_dim=hd, layer=0, rope=table,
+                           n_q_heads=hq)
+    torch.cuda.synchronize()
+    q_rot = attn_oracle.apply_rope(qkv[:, : hq * hd].cpu().float().view(T, hq, hd), pos, theta)
+    ref = attn_oracle.prefix_prefill(q_rot, pool.cpu(), requests, 0)
+    err = (out.cpu().float() - ref).abs().max().item()
+    assert err <= ATTN_ATOL, err
+    # K/V-only write: q is not rotated or written, K/V land in the pool rotated
+    assert T <= nb * bt
+    slots = torch.arange(T, dtype=torch.int32, device="cuda")  # token t -> block t//bt, row t%bt
+    pool2 = torch.zeros_like(pool)
+    kernels.kv_write_rope(None, qkv[:, hq * hd:(hq + hkv) * hd], qkv[:, (hq + hkv) * hd:], None,
+                          pos.cuda(), slots, pool2.data_ptr(), block_tokens=bt, n_layers=L,
+                          n_kv_heads=hkv, head_dim=hd, layer=0, rope_theta=theta, n_q_heads=hq)
+    torch.cuda.synchronize()
+    k_ref = attn_oracle.apply_rope(qkv[:, hq * hd:(hq + hkv) * hd].cpu().float().view(T, hkv, hd),
+                                   pos, theta)
+    pc = pool2.cpu()
+    for t in (0, T // 2, T - 1):
+        assert (pc[t // bt, 0, 0, :, t % bt, :].float() - k_ref[t]).abs().max().item() < 0.05

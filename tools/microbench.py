@@ -158,7 +158,10 @@ def bench_attn():
         ("mistral mixed step", 32, 8, 64, [(0, 1056)] * 26 + [(512, 544)] * 26 + [(1024, 32)] * 12),
         ("llama2 miss a0 b544 x16", 32, 32, 64, [(0, 544)] * 16),
     ]
+    only = os.environ.get("MB_CASE")
     for name, hq, hkv, bt, reqs in cases:
+        if only and only not in name:
+            continue
         hd, L = 128, 2
         total_slots = sum(-(-(a + b) // bt) for a, b in reqs)
         nb = total_slots + 8
@@ -183,6 +186,33 @@ def bench_attn():
         emit(kind="prefix_prefill", case=name, ms=med, tflops=flops / med / 1e9,
              frac_tc=flops / med / 1e9 / tc, kv_gbs=kv_bytes / med / 1e6, work_items=plan.n_work,
              kv_tiles=plan.kv_tiles)
+        # fused Q-RoPE: raw Q columns of a QKV row, rotated in shared memory
+        qkv = torch.randn((T, (hq + 2 * hkv) * hd), device="cuda").to(torch.bfloat16)
+        rope = kernels.rope_table(plan.max_pos + 1, hd, 1e6)
+        fn = lambda: kernels.prefix_prefill(qkv[:, : hq * hd], o, plan, pool.data_ptr(), nb,
+                                            block_tokens=bt, n_layers=L, n_kv_heads=hkv,
+                                            head_dim=hd, layer=1, rope=rope, n_q_heads=hq)
+        med, best = timed(fn)
+        emit(kind="prefix_prefill_rope", case=name, ms=med, tflops=flops / med / 1e9,
+             frac_tc=flops / med / 1e9 / tc)
+        fn = lambda: kernels.prefix_prefill(q, o, plan, pool.data_ptr(), nb,
+                                            block_tokens=bt, n_layers=L, n_kv_heads=hkv,
+                                            head_dim=hd, layer=1, rope=rope, n_q_heads=hq)
+        med, best = timed(fn)
+        emit(kind="prefix_prefill_rope_contig_q", case=name, ms=med, tflops=flops / med / 1e9)
+        pos_t = torch.cat([a + torch.arange(b) for a, b in reqs]).to(torch.int32).cuda()
+        slots = torch.arange(T, dtype=torch.int32, device="cuda")
+        x = qkv
+        k = x[:, hq * hd:(hq + hkv) * hd]
+        v = x[:, (hq + hkv) * hd:]
+        qr = torch.empty((T, hq, hd), dtype=torch.bfloat16, device="cuda")
+        for mode, qq, qo in (("qkv", x[:, : hq * hd], qr), ("kv_only", None, None)):
+            fn = lambda: kernels.kv_write_rope(qq, k, v, qo, pos_t, slots, pool.data_ptr(),
+                                               block_tokens=bt, n_layers=L, n_kv_heads=hkv,
+                                               head_dim=hd, layer=1, rope_theta=1e6, n_q_heads=hq)
+            med, best = timed(fn)
+            nbytes = T * hd * 2 * (2 * hkv * 2 + (2 * hq if qq is not None else 0))
+            emit(kind="kv_write_rope", mode=mode, case=name, ms=med, gbs=nbytes / med / 1e6)
         del pool
 
 

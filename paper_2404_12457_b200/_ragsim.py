@@ -31,7 +31,7 @@ def import_ragsim():
             return importlib.import_module("ragsim")
     raise ImportError(
         "ragsim (the reference host-side API) is not importable; install it with "
-        "`pip install --no-index --target baseline/_ref <reference>/pkg`"
+        "`pip install --no-index --no-build-isolation --no-deps --target baseline/_ref <copy of reference>/pkg`"
     )
 
 

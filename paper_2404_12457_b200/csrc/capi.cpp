@@ -93,9 +93,10 @@ int rcb_attn_plan(const int32_t* req_meta, int32_t n_req, const int32_t* blk_val
   if (n_kv_heads <= 0 || n_q_heads % n_kv_heads != 0 || 128 % (n_q_heads / n_kv_heads) != 0)
     return rcb::set_error(RCB_ERR_ARG, "unsupported head grouping");
   const int g = n_q_heads / n_kv_heads;
-  const int tq = 128 / g;
+  const int tq = 128 / g;  // tokens per 128-row query tile
   struct Item {
-    int32_t r, qt, h, tiles;
+    int32_t r, qp, h, n0, n1;
+    int32_t tiles() const { return n0 > n1 ? n0 : n1; }
   };
   const int kItemInts = 8;
   std::vector<Item> items;
@@ -106,11 +107,11 @@ int rcb_attn_plan(const int32_t* req_meta, int32_t n_req, const int32_t* blk_val
     const int32_t nb = req_meta[r * 5 + 4];
     if (q_len <= 0) continue;
     if (nb <= 0) return rcb::set_error(RCB_ERR_ARG, "request with queries but no blocks");
-    const int32_t n_qt = (q_len + tq - 1) / tq;
-    for (int32_t qt = 0; qt < n_qt; ++qt) {
+    // KV tiles (128 key slots) query tile qt needs: up to the slot of its last token
+    auto tiles_of = [&](int32_t qt) -> int32_t {
+      if (qt * tq >= q_len) return 0;
       const int32_t max_qp = q_pos0 + std::min(q_len, (qt + 1) * tq) - 1;
-      // last block whose start <= max_qp
-      int32_t lo = 0, hi = nb - 1;
+      int32_t lo = 0, hi = nb - 1;  // last block whose start <= max_qp
       while (lo < hi) {
         const int32_t mid = (lo + hi + 1) / 2;
         if (blk_pos[b0 + mid] <= max_qp) lo = mid;
@@ -118,22 +119,27 @@ int rcb_attn_plan(const int32_t* req_meta, int32_t n_req, const int32_t* blk_val
       }
       const int32_t off = std::min(blk_valid[b0 + lo] - 1, max_qp - blk_pos[b0 + lo]);
       const int32_t slot = lo * block_tokens + std::max(0, off);
-      const int32_t tiles = slot / 128 + 1;
-      for (int32_t h = 0; h < n_kv_heads; ++h) items.push_back({r, qt, h, tiles});
+      return slot / 128 + 1;
+    };
+    const int32_t n_pairs = (q_len + 2 * tq - 1) / (2 * tq);
+    for (int32_t qp = 0; qp < n_pairs; ++qp) {
+      const int32_t n0 = tiles_of(2 * qp), n1 = tiles_of(2 * qp + 1);
+      if (n0 > 0xffff || n1 > 0xffff) return rcb::set_error(RCB_ERR_ARG, "sequence too long");
+      for (int32_t h = 0; h < n_kv_heads; ++h) items.push_back({r, qp, h, n0, n1});
     }
   }
   // L2 locality: the ~148 CTAs of a persistent launch take consecutive items,
   // so keep all q-tiles of one (request, kv head) adjacent — they re-read the
   // same K/V pages.  Requests go heaviest first, q-tiles longest first.
   std::vector<int64_t> req_work(n_req, 0);
-  for (const Item& it : items) req_work[it.r] += it.tiles;
+  for (const Item& it : items) req_work[it.r] += it.n0 + it.n1;
   std::stable_sort(items.begin(), items.end(), [&](const Item& a, const Item& b) {
     if (a.r != b.r) {
       if (req_work[a.r] != req_work[b.r]) return req_work[a.r] > req_work[b.r];
       return a.r < b.r;
     }
     if (a.h != b.h) return a.h < b.h;
-    return a.tiles > b.tiles;
+    return a.n0 + a.n1 > b.n0 + b.n1;
   });
   if (n_work_out) *n_work_out = static_cast<int32_t>(items.size());
   if (static_cast<int32_t>(items.size()) > cap)
@@ -146,9 +152,9 @@ int rcb_attn_plan(const int32_t* req_meta, int32_t n_req, const int32_t* blk_val
     w[2] = m[2];  // q_pos0
     w[3] = m[3];  // blk_begin
     w[4] = m[4];  // blk_count
-    w[5] = items[i].qt;
+    w[5] = items[i].qp;
     w[6] = items[i].h;
-    w[7] = items[i].tiles;
+    w[7] = items[i].n0 | (items[i].n1 << 16);
   }
   return RCB_OK;
 }

@@ -99,7 +99,7 @@ class AttnPlan:
         valid_np = np.asarray(valid, dtype=np.int32)
         pos_np = np.asarray(pos, dtype=np.int32)
         g = n_q_heads // n_kv_heads
-        cap = sum(max(0, -(-r[0] // (128 // g))) for r in requests) * n_kv_heads + 1
+        cap = sum(max(0, -(-r[0] // (256 // g))) for r in requests) * n_kv_heads + 1
         work = np.zeros(cap * 8, dtype=np.int32)
         n_work = np.zeros(1, dtype=np.int32)
         check(load().rcb_attn_plan(
@@ -108,8 +108,13 @@ class AttnPlan:
             work.ctypes.data_as(_lib._p32), cap, n_work.ctypes.data_as(_lib._p32)),
             "rcb_attn_plan")
         self.n_work = int(n_work[0])
+        # {q_start, q_len, q_pos0, blk_begin, blk_count, q_pair, kv_head, n0 | n1 << 16}:
+        # an item = two adjacent 128-row query tiles sharing each KV tile it loads
         self.work_host = work[: self.n_work * 8].reshape(-1, 8)
-        self.kv_tiles = int(self.work_host[:, 7].sum()) if self.n_work else 0
+        self.tiles_q0 = self.work_host[:, 7] & 0xFFFF
+        self.tiles_q1 = self.work_host[:, 7] >> 16
+        self.kv_tiles = int(np.maximum(self.tiles_q0, self.tiles_q1).sum()) if self.n_work else 0
+        self.mma_tiles = int((self.tiles_q0 + self.tiles_q1).sum()) if self.n_work else 0
         # work items first: the kernel reads them as int4 (16-byte aligned)
         pack = np.concatenate([work[: self.n_work * 8], meta_np, np.asarray(ids, dtype=np.int32),
                                valid_np, pos_np])

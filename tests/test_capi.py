@@ -45,19 +45,23 @@ def test_attn_plan_host_logic():
     # two requests: a cached 1024-token prefix + 32 prompt tokens, and a full miss
     reqs = [(32, 1024, list(range(66)), [16] * 66), (544, 0, list(range(34)), [16] * 34)]
     plan = kernels.AttnPlan(reqs, block_tokens=16, n_q_heads=32, n_kv_heads=8, device="cpu")
-    w = plan.work_host  # {q_start, q_len, q_pos0, blk_begin, blk_count, q_tile, kv_head, n}
-    # GQA-4: 32 tokens per query tile -> 1 tile for req 0, 17 for req 1, x 8 kv heads
-    assert plan.n_work == (1 + 17) * 8
-    # L2 order: heaviest request first (req 1: 17 q-tiles), grouped by kv head,
-    # longest q-tile first within a group
-    assert w[0, 0] == 32 and w[0, 6] == 0 and w[0, 7] == 5
+    w = plan.work_host  # {q_start, q_len, q_pos0, blk_begin, blk_count, q_pair, kv_head, n0|n1<<16}
+    n0, n1 = plan.tiles_q0, plan.tiles_q1
+    # GQA-4: 32 tokens per query tile, two tiles per item -> 1 pair for req 0, 9 for req 1
+    assert plan.n_work == (1 + 9) * 8
+    # L2 order: heaviest request first (req 1), grouped by kv head, longest pair first
+    assert w[0, 0] == 32 and w[0, 6] == 0 and (n0[0], n1[0]) == (4, 4)
     for h in range(8):
-        grp = w[(w[:, 0] == 32) & (w[:, 6] == h)]
-        assert list(grp[:, 7]) == sorted(grp[:, 7], reverse=True)
-    r0 = w[w[:, 0] == 0]  # request 0 starts at query row 0
-    assert set(r0[:, 7]) == {9}  # 1056 slots -> 9 key tiles
-    assert set(map(tuple, r0[:, :5])) == {(0, 32, 1024, 0, 66)}
-    r1 = w[w[:, 0] == 32]
-    # causal: query tile t covers tokens [32t, 32t+32) -> needs key tile (32t+31)//128
-    assert sorted(set(zip(r1[:, 5], r1[:, 7]))) == [(t, (32 * t + 31) // 128 + 1) for t in range(17)]
-    assert np.all(np.bincount(r1[:, 6]) == 17)
+        sel = (w[:, 0] == 32) & (w[:, 6] == h)
+        tot = list(n0[sel] + n1[sel])
+        assert tot == sorted(tot, reverse=True)
+    r0 = (w[:, 0] == 0)  # request 0 starts at query row 0: one tile, Q1 empty
+    assert set(n0[r0]) == {9} and set(n1[r0]) == {0}  # 1056 slots -> 9 key tiles
+    assert set(map(tuple, w[r0, :5])) == {(0, 32, 1024, 0, 66)}
+    r1 = (w[:, 0] == 32)
+    # causal: query tile t covers tokens [32t, 32t+32) -> needs key tile (32t+31)//128;
+    # the last pair (tokens 512..543) has an empty Q1
+    got = sorted(set(zip(w[r1, 5], n0[r1], n1[r1])))
+    need = lambda t: (32 * t + 31) // 128 + 1 if 32 * t < 544 else 0
+    assert got == [(p, need(2 * p), need(2 * p + 1)) for p in range(9)]
+    assert np.all(np.bincount(w[r1, 6]) == 9)

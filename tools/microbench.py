@@ -157,6 +157,7 @@ def bench_attn():
         ("mistral miss a0 b1056 x16", 32, 8, 64, [(0, 1056)] * 16),
         ("mistral mixed step", 32, 8, 64, [(0, 1056)] * 26 + [(512, 544)] * 26 + [(1024, 32)] * 12),
         ("llama2 miss a0 b544 x16", 32, 32, 64, [(0, 544)] * 16),
+        ("mistral long a4096 b256 x32", 32, 8, 64, [(4096, 256)] * 32),
     ]
     only = os.environ.get("MB_CASE")
     for name, hq, hkv, bt, reqs in cases:

@@ -28,6 +28,7 @@ import json
 import math
 import os
 import statistics
+import threading
 import subprocess
 import sys
 import time
@@ -66,45 +67,54 @@ from paper_2404_12457_b200.dist import Dist, route, shard_bounds  # noqa: E402
 
 # ---------------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clocks + throttle reasons sampled DURING the timed region: an NVML thread at
+    ~5 ms (the timed region can be a fraction of a second), nvidia-smi as fallback."""
+
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+               ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4))
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.path = f"/tmp/rcb_clocks_{os.getpid()}.csv"
+        self.samples: list[tuple[float, int]] = []
+        self.smax = None
+        self.thread = None
+        self.stop_flag = threading.Event()
+        self.error = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except Exception:
-            self.proc = None
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.smax = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+
+            def sample():
+                self.samples.append((float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)),
+                                     int(get_reasons(h))))
+
+            sample()  # NVML is live before the timed region starts
+
+            def loop():
+                while not self.stop_flag.wait(0.005):
+                    sample()
+
+            self.thread = threading.Thread(target=loop, daemon=True)
+            self.thread.start()
+        except Exception as exc:  # no NVML: the caller still gets a line, marked
+            self.error = f"nvml unavailable: {exc}"[:80]
 
     def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        self.proc.wait()
-        sm, smax, reasons = [], 0.0, set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for line in open(self.path):
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax = max(smax, float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if self.thread is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.error or "no samples"]}
+        self.stop_flag.set()
+        self.thread.join()
+        loaded = self.samples[1:] or self.samples  # drop the pre-region sample
+        reasons = sorted({n for _, r in loaded for n, bit in self.REASONS if r & bit})
+        return {"sm_mhz": statistics.median(c for c, _ in loaded), "sm_max_mhz": self.smax,
+                "reasons": reasons, "samples": len(loaded), "source": "nvml, 5 ms"}
 
 
 def peaks():

@@ -27,6 +27,7 @@ Transition map:
 
 from __future__ import annotations
 
+import heapq
 import itertools
 from dataclasses import dataclass, field
 
@@ -71,15 +72,76 @@ def _pool_call(fn, *args):
         raise CacheError(str(exc)) from exc
 
 
+class _IndexedLeaves(set):
+    """The reference's tier-leaf set plus a lazy min-heap on the policy's eviction key.
+
+    ``KnowledgeTree._min_leaf`` (tree.py:407-411) scans every leaf per victim: with a
+    1.1M-token GPU tier that scan is ~85% of the host time of a step.  The eviction key
+    (priority, -size, doc, serial) (policies.py:46-50) ends in the node's unique serial, so
+    it is a total order and the heap minimum is exactly the victim ``min()`` picks.  The
+    reference mutates the set with add/discard only; keys change only in update_node
+    (tree.py:233-246), which re-pushes the node.  Stale entries (left the set, or an old
+    key) are dropped when they surface."""
+
+    def __init__(self, items, key) -> None:
+        super().__init__(items)
+        self.key = key
+        self.heap: list = []
+        self._seq = itertools.count()
+        for node in items:
+            self.push(node)
+
+    def push(self, node) -> None:
+        heapq.heappush(self.heap, (self.key(node), next(self._seq), node))
+
+    def add(self, node) -> None:
+        if node not in self:
+            super().add(node)
+            self.push(node)
+
+    def min_unpinned(self):
+        heap, aside, found = self.heap, [], None
+        while heap:
+            k, _, node = heap[0]
+            if node not in self or k != self.key(node):
+                heapq.heappop(heap)
+            elif node.pinned:
+                aside.append(heapq.heappop(heap))
+            else:
+                found = node
+                break
+        for entry in aside:
+            heapq.heappush(heap, entry)
+        if len(heap) > 64 and len(heap) > 4 * len(self):
+            self.heap = [(self.key(n), next(self._seq), n) for n in self]
+            heapq.heapify(self.heap)
+        return found
+
+
 class TieredKnowledgeTree(KnowledgeTree):
     """ragsim KnowledgeTree whose tier transitions drive a block pool."""
 
     def __init__(self, gpu_capacity: int, host_capacity: int, policy=None,
-                 frequency_decay: float = 1.0, *, pool) -> None:
+                 frequency_decay: float = 1.0, *, pool, indexed_leaves: bool = True) -> None:
         super().__init__(gpu_capacity, host_capacity, policy=policy,
                          frequency_decay=frequency_decay)
         self.pool = pool
         self.gen_ctx: GenContext | None = None
+        if indexed_leaves:
+            self._gpu_leaves = _IndexedLeaves(self._gpu_leaves, self.policy.eviction_key)
+            self._host_leaves = _IndexedLeaves(self._host_leaves, self.policy.eviction_key)
+
+    # -- victim selection (same victims as tree.py:407-411, without the scan) -------
+    def _min_leaf(self, leaves):
+        if isinstance(leaves, _IndexedLeaves):
+            return leaves.min_unpinned()
+        return super()._min_leaf(leaves)
+
+    def update_node(self, node, *args, **kwargs) -> None:
+        super().update_node(node, *args, **kwargs)
+        for leaves in (self._gpu_leaves, self._host_leaves):
+            if isinstance(leaves, _IndexedLeaves) and node in leaves:
+                leaves.push(node)
 
     # -- eviction side ------------------------------------------------------
     def _demote_from_gpu(self, node) -> None:

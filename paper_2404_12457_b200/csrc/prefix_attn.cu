@@ -37,9 +37,12 @@ constexpr int kThreads = 512;
 constexpr int kRows = 128;
 constexpr int kKeys = 128;  // key slots per KV tile
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
-// exp2 on the FMA pipe (cubic polynomial) for kPolyCols of every 8 score columns
+// exp2 on the FMA/ALU pipes (magic-add rounding + cubic) for kPolyCols of every 8 score
+// columns.  Measured on B200: 2 of 8 is fastest (long prefix 1106 -> 1155 TFLOP/s, mixed
+// step 859 -> 893); 4 of 8 loses (the FMA pipe then saturates).  An earlier variant that
+// rounded with floorf (FRND, not on the FMA pipe) gained nothing.
 #ifndef RCB_POLY_COLS
-#define RCB_POLY_COLS 0
+#define RCB_POLY_COLS 2
 #endif
 constexpr int kPolyCols = RCB_POLY_COLS;
 

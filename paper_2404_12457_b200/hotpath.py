@@ -199,18 +199,21 @@ class HotPath:
         q0 = 0
         for a in plan.admissions:
             nb_prefix = sum(-(-n.size // bt) for n in a.matched)
-            seg_blocks = a.blocks[nb_prefix:]
-            seg_valid = a.valid[nb_prefix:]
-            t = 0
-            for b, v in zip(seg_blocks, seg_valid):
-                for o in range(v):
-                    slots.append(b * bt + o)
-                    pos.append(a.alpha + t)
-                    t += 1
-            assert t == a.beta
+            seg_blocks = np.asarray(a.blocks[nb_prefix:], dtype=np.int64)
+            seg_valid = np.asarray(a.valid[nb_prefix:], dtype=np.int64)
+            if int(seg_valid.sum()) != a.beta:
+                raise AssertionError("suffix segments do not cover beta tokens")
+            # token t of the suffix -> pool slot block*bt + offset within its block
+            starts = np.cumsum(seg_valid) - seg_valid
+            off = np.arange(a.beta) - np.repeat(starts, seg_valid)
+            slots.append(np.repeat(seg_blocks * bt, seg_valid) + off)
+            pos.append(a.alpha + np.arange(a.beta))
             q0 += a.beta
             last.append(q0 - 1)
-        arr = torch.from_numpy(np.asarray(pos + slots + last, dtype=np.int32)).to(device)
+        pos = np.concatenate(pos) if pos else np.zeros(0, np.int64)
+        slots = np.concatenate(slots) if slots else np.zeros(0, np.int64)
+        arr = kernels._upload(np.concatenate([pos, slots, np.asarray(last, np.int64)])
+                              .astype(np.int32), device)
         n = len(pos)
         plan.dev = {"attn": attn, "pos": arr[:n], "slots": arr[n:2 * n],
                     "last": arr[2 * n:].long(), "flops": attention_flops(self.shape, reqs)}

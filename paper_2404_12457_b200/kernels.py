@@ -28,6 +28,15 @@ def _stream(stream) -> int:
     return _lib.stream_handle(stream)
 
 
+def _upload(arr: np.ndarray, device) -> torch.Tensor:
+    """Host array -> device without a stream sync: a pageable copy would wait for the
+    work already queued (e.g. the previous step's prefill) before returning."""
+    t = torch.from_numpy(arr)
+    if torch.device(device).type != "cuda":
+        return t.to(device)
+    return t.pin_memory().to(device, non_blocking=True)
+
+
 def block_copy(src_base: int, dst_base: int, block_bytes: int, pairs: torch.Tensor,
                stream=None) -> None:
     """dst[pairs[i,1]] = src[pairs[i,0]] for block_bytes-sized blocks (device/mapped ptrs)."""
@@ -118,7 +127,7 @@ class AttnPlan:
         # work items first: the kernel reads them as int4 (16-byte aligned)
         pack = np.concatenate([work[: self.n_work * 8], meta_np, np.asarray(ids, dtype=np.int32),
                                valid_np, pos_np])
-        self._buf = torch.from_numpy(pack).to(device)
+        self._buf = _upload(pack, device)
         o = 0
         self.work = self._buf[o:o + self.n_work * 8]; o += self.n_work * 8
         self.meta = self._buf[o:o + meta_np.size]; o += meta_np.size

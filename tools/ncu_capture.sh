@@ -11,7 +11,8 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 ncu --set full --clock-control none --import-source on -k regex:prefix_prefill -s 5 -c 1 \
     -o gpurun_out/${TAG}_attn_bench python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-ttft > /dev/null 2>&1
 # 3. full captures of each hot kernel (microbench shapes)
-ncu --set full --clock-control none --import-source on -k regex:prefix_prefill -s 4 -c 1 \
+# (the mixed-step case only: 2 plain launches, then the fused-RoPE one is captured)
+MB_CASE="mixed step" ncu --set full --clock-control none --import-source on -k regex:prefix_prefill -s 2 -c 1 \
     -o gpurun_out/${TAG}_attn_mixed python tools/microbench.py attn --ncu > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:topk_scan -s 0 -c 1 \
     -o gpurun_out/${TAG}_retrieval_scan python tools/microbench.py retrieval --ncu > /dev/null 2>&1

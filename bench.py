@@ -117,6 +117,20 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(loaded), "source": "nvml, 5 ms"}
 
 
+NCU_TAG = "r1b"  # profiles/<tag>_ncu_summary.json: captures of the current kernels
+
+
+def ncu_traffic(capture: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one captured launch, or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                        f"{NCU_TAG}_ncu_summary.json")
+    try:
+        k = json.load(open(path))["kernels"][capture]
+        return float(k["dram_traffic_bytes"]), f"ncu --set full, {os.path.basename(path)}:{capture}"
+    except (OSError, KeyError, ValueError):
+        return None, None
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -341,6 +355,14 @@ def run_ours(args, dist: Dist):
     hbm_peak, tc_peak, peak_kind = peaks()
     attn_mean_ms = sum(attn_ms) / len(attn_ms)
     achieved_tf = (sum(flops) / len(flops)) / (attn_mean_ms / 1e3) / 1e12
+    # algorithmic bytes per launch: KV of alpha+beta tokens for one layer +
+    # Q read + O write; traffic = DRAM bytes of the same launch from the committed ncu
+    # --set full capture of the bench step (profiles/<tag>_ncu_summary.json, attn_bench)
+    attn_bytes = sum(
+        sum((a.alpha + a.beta) * 2 * shape.n_kv_heads * shape.head_dim * 2
+            + 4 * a.beta * shape.n_q_heads * shape.head_dim for a in plans[W + i].admissions)
+        for i in range(K)) / K
+    traffic, traffic_src = ncu_traffic("attn_bench")
     scan_ms = [a.elapsed_time(b) for a, b in scan_ev]
     scan_gbs = retr.bytes_per_scan / (sum(scan_ms) / len(scan_ms) / 1e3) / 1e9 if scan_ms else 0.0
     d2h = st1["d2h_bytes"] - st0["d2h_bytes"]
@@ -401,7 +423,9 @@ def run_ours(args, dist: Dist):
                 "peak": tc_peak,
                 "unit": "TFLOP/s",
                 "frac": round(achieved_tf / tc_peak, 4),
-                "traffic": None,
+                "traffic": traffic,
+                "traffic_source": traffic_src,
+                "algorithmic_bytes_per_launch": attn_bytes,
                 "peak_source": f"{peak_kind} bf16 sustained",
                 "launch_ms_mean": round(attn_mean_ms, 4),
                 "flops_per_launch": sum(flops) / len(flops),

@@ -96,7 +96,7 @@ int rcb_attn_plan(const int32_t* req_meta, int32_t n_req, const int32_t* blk_val
   const int tq = 128 / g;  // tokens per 128-row query tile
   struct Item {
     int32_t r, qp, h, n0, n1;
-    int32_t tiles() const { return n0 > n1 ? n0 : n1; }
+    bool half0, half1;  // the tile's last KV tile needs only its first 64 key slots
   };
   const int kItemInts = 8;
   std::vector<Item> items;
@@ -107,8 +107,10 @@ int rcb_attn_plan(const int32_t* req_meta, int32_t n_req, const int32_t* blk_val
     const int32_t nb = req_meta[r * 5 + 4];
     if (q_len <= 0) continue;
     if (nb <= 0) return rcb::set_error(RCB_ERR_ARG, "request with queries but no blocks");
-    // KV tiles (128 key slots) query tile qt needs: up to the slot of its last token
-    auto tiles_of = [&](int32_t qt) -> int32_t {
+    // KV tiles (128 key slots) query tile qt needs: up to the slot of its last token;
+    // *half: that slot lies in the first 64 slots of the last tile
+    auto tiles_of = [&](int32_t qt, bool* half) -> int32_t {
+      *half = false;
       if (qt * tq >= q_len) return 0;
       const int32_t max_qp = q_pos0 + std::min(q_len, (qt + 1) * tq) - 1;
       int32_t lo = 0, hi = nb - 1;  // last block whose start <= max_qp
@@ -119,13 +121,15 @@ int rcb_attn_plan(const int32_t* req_meta, int32_t n_req, const int32_t* blk_val
       }
       const int32_t off = std::min(blk_valid[b0 + lo] - 1, max_qp - blk_pos[b0 + lo]);
       const int32_t slot = lo * block_tokens + std::max(0, off);
+      *half = (slot % 128) < 64;
       return slot / 128 + 1;
     };
     const int32_t n_pairs = (q_len + 2 * tq - 1) / (2 * tq);
     for (int32_t qp = 0; qp < n_pairs; ++qp) {
-      const int32_t n0 = tiles_of(2 * qp), n1 = tiles_of(2 * qp + 1);
-      if (n0 > 0xffff || n1 > 0xffff) return rcb::set_error(RCB_ERR_ARG, "sequence too long");
-      for (int32_t h = 0; h < n_kv_heads; ++h) items.push_back({r, qp, h, n0, n1});
+      bool h0 = false, h1 = false;
+      const int32_t n0 = tiles_of(2 * qp, &h0), n1 = tiles_of(2 * qp + 1, &h1);
+      if (n0 > 0x7fff || n1 > 0x7fff) return rcb::set_error(RCB_ERR_ARG, "sequence too long");
+      for (int32_t h = 0; h < n_kv_heads; ++h) items.push_back({r, qp, h, n0, n1, h0, h1});
     }
   }
   // L2 locality: the ~148 CTAs of a persistent launch take consecutive items,
@@ -154,7 +158,12 @@ int rcb_attn_plan(const int32_t* req_meta, int32_t n_req, const int32_t* blk_val
     w[4] = m[4];  // blk_count
     w[5] = items[i].qp;
     w[6] = items[i].h;
-    w[7] = items[i].n0 | (items[i].n1 << 16);
+    // n0 | half0 << 15 | n1 << 16 | half1 << 31
+    const uint32_t packed = static_cast<uint32_t>(items[i].n0) |
+                            (static_cast<uint32_t>(items[i].half0) << 15) |
+                            (static_cast<uint32_t>(items[i].n1) << 16) |
+                            (static_cast<uint32_t>(items[i].half1) << 31);
+    w[7] = static_cast<int32_t>(packed);
   }
   return RCB_OK;
 }

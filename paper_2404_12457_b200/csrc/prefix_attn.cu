@@ -72,14 +72,18 @@ struct Smem {
 };
 
 // Work items are self-contained (no dependent loads at item start):
-//   {q_start, q_len, q_pos0, blk_begin, blk_count, q_pair, kv_head, n0 | n1 << 16}
-// n_w = KV tiles query tile w needs; the item runs max(n0, n1) KV steps.
+//   {q_start, q_len, q_pos0, blk_begin, blk_count, q_pair, kv_head,
+//    n0 | half0 << 15 | n1 << 16 | half1 << 31}
+// n_w = KV tiles query tile w needs; the item runs max(n0, n1) KV steps.  half_w: the last
+// of them needs only its first 64 key slots -> QK with N = 64, PV with K = 64, and the
+// softmax does one 64-column chunk.
 //   pair item  (n1 > 0): softmax WG w owns query tile Q_w over steps j < n_w
 //   split item (n1 == 0, a lone query tile): WG w owns the steps j with j % 2 == w of Q0,
 //              each WG keeps its own (m, l, O_w) and the epilogue merges the two
 constexpr int kItemInts = 8;
 struct Item {
   int q_start, q_len, q_pos0, blk_begin, blk_count, qp, kvh, n0, n1;
+  bool h0, h1;
   __device__ __forceinline__ bool split() const { return n1 == 0; }
   __device__ __forceinline__ int n() const { return n0 > n1 ? n0 : n1; }
   // WG w works on step j
@@ -97,12 +101,18 @@ struct Item {
   }
   // query tile WG w reads
   __device__ __forceinline__ int qtile(int w) const { return split() ? 0 : w; }
+  // step j of WG w covers only the first 64 key slots
+  __device__ __forceinline__ bool half(int w, int j) const {
+    return split() ? (h0 && j == n0 - 1) : (w ? (h1 && j == n1 - 1) : (h0 && j == n0 - 1));
+  }
 };
 
 __device__ __forceinline__ Item load_item(const int* __restrict__ work, int idx) {
   const int4 a = *reinterpret_cast<const int4*>(work + idx * kItemInts);
   const int4 b = *reinterpret_cast<const int4*>(work + idx * kItemInts + 4);
-  return Item{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w & 0xffff, b.w >> 16};
+  const uint32_t p = static_cast<uint32_t>(b.w);
+  return Item{a.x, a.y, a.z, a.w, b.x, b.y, b.z, static_cast<int>(p & 0x7fffu),
+              static_cast<int>((p >> 16) & 0x7fffu), ((p >> 15) & 1u) != 0, (p >> 31) != 0};
 }
 
 // Persistent: CTA c serves work items c, c + grid, ... (heaviest first).  The KV step
@@ -244,6 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ MMA issuer
     if (elect_one()) {
       constexpr uint32_t idesc_qk = idesc_bf16_f32(128, kKeys, 0, 0);
+      constexpr uint32_t idesc_qk_half = idesc_bf16_f32(128, kKeys / 2, 0, 0);
       constexpr uint32_t idesc_pv = idesc_bf16_f32(128, HD, 0, 1);
       const uint32_t q_base = smem_u32(sQ);
       const uint32_t kv_base = smem_u32(sKV);
@@ -251,6 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int oc[2] = {0, 0};  // items with a non-empty Q_w so far (O_w phases)
       // the previous step's pending PVs
       bool p_has[2] = {false, false}, p_last[2] = {false, false}, p_first[2] = {false, false};
+      bool p_half[2] = {false, false};
       int p_c[2] = {0, 0}, p_vu = 0;
       bool p_any = false, p_v_ready = false;
       auto issue_pv = [&](int w) {
@@ -263,8 +275,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&bar[kPFull0 + w], p_c[w] & 1);
         tc_fence_after();
         const int st = p_vu % NS;
+        const int nkk = p_half[w] ? kKeys / 32 : kKeys / 16;  // a half tile: 64 keys
 #pragma unroll
         for (int kk = 0; kk < kKeys / 16; ++kk) {
+          if (kk >= nkk) break;
           // A = P_w (bf16 pairs over S_w's first 64 columns); V tile is [half][128 keys][64]:
           // MN-major, halves 16 KB apart (LBO)
           const uint64_t b = sw128_desc(kv_base + st * S::kKV + kk * 2048, 16384, 1024);
@@ -276,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ++oc[w];
         }
       };
-      auto issue_qk = [&](int w, int qt, int ku) {  // qt: Q buffer [item parity][tile]
+      auto issue_qk = [&](int w, int qt, int ku, bool half) {  // qt: Q buffer [parity][tile]
         const int st = ku % NS;
         const uint32_t d = tmem + w * kKeys;
 #pragma unroll
@@ -284,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
           const uint64_t a = sw128_desc(q_base + qt * S::kQ + off, 16, 1024);
           const uint64_t b = sw128_desc(kv_base + st * S::kKV + off, 16, 1024);
-          umma_bf16_ss(d, a, b, idesc_qk, kk > 0 ? 1u : 0u);
+          umma_bf16_ss(d, a, b, half ? idesc_qk_half : idesc_qk, kk > 0 ? 1u : 0u);
         }
         umma_commit(&bar[kSFull0 + w]);
         ++c[w];
@@ -312,14 +326,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int pc0 = c[0];
           if (h0) {
             need_k();
-            issue_qk(0, qb * 2, ku);
+            issue_qk(0, qb * 2, ku, it.half(0, j));
           }
           if (p_has[1]) issue_pv(1);
           if (p_any) umma_commit(&kv_empty[p_vu % NS]);  // V(s-1) no longer read
           const int pc1 = c[1];
           if (h1) {
             need_k();
-            issue_qk(1, qb * 2 + it.qtile(1), ku);
+            issue_qk(1, qb * 2 + it.qtile(1), ku, it.half(1, j));
           }
           umma_commit(&kv_empty[ku % NS]);  // K(s) no longer read
           if (j == n - 1) umma_commit(&bar[kQEmpty0 + qb]);  // Q tiles no longer read
@@ -335,6 +349,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           p_first[1] = (j == it.first(1));
           p_last[0] = (j == it.last(0));
           p_last[1] = (j == it.last(1));
+          p_half[0] = it.half(0, j);
+          p_half[1] = it.half(1, j);
         }
       }
       if (p_any) {
@@ -385,12 +401,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&bar[kSFull0 + wg], c & 1);
         tc_fence_after();
         const bool masked = !all_valid || max_pos > qp;
+        const bool half = it.half(wg, j);  // only S columns [0, 64) were computed
         // Two 64-column chunks against the running max m (within 2^8 of the true row max:
         // a chunk that exceeds m + 2^8 rescales O, l and the already-packed P of chunk 0).
         // P of chunk c (bf16 pairs) goes to S columns [32c, 32c + 32): chunk 0's own
         // columns, then chunk 0's (already consumed) columns for chunk 1.
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
+          if (ch == 1 && half) break;
           {
             uint32_t r[kKeys / 2];
             tmem_ld64(s_col + ch * (kKeys / 2), r);

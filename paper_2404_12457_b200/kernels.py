@@ -117,11 +117,15 @@ class AttnPlan:
             work.ctypes.data_as(_lib._p32), cap, n_work.ctypes.data_as(_lib._p32)),
             "rcb_attn_plan")
         self.n_work = int(n_work[0])
-        # {q_start, q_len, q_pos0, blk_begin, blk_count, q_pair, kv_head, n0 | n1 << 16}:
-        # an item = two adjacent 128-row query tiles sharing each KV tile it loads
+        # {q_start, q_len, q_pos0, blk_begin, blk_count, q_pair, kv_head,
+        #  n0 | half0 << 15 | n1 << 16 | half1 << 31}: an item = two adjacent 128-row query
+        # tiles sharing each KV tile it loads; half_w: Q_w's last KV tile needs 64 slots
         self.work_host = work[: self.n_work * 8].reshape(-1, 8)
-        self.tiles_q0 = self.work_host[:, 7] & 0xFFFF
-        self.tiles_q1 = self.work_host[:, 7] >> 16
+        packed = self.work_host[:, 7].view(np.uint32)
+        self.tiles_q0 = (packed & 0x7FFF).astype(np.int64)
+        self.tiles_q1 = ((packed >> 16) & 0x7FFF).astype(np.int64)
+        self.half_q0 = ((packed >> 15) & 1).astype(bool)
+        self.half_q1 = ((packed >> 31) & 1).astype(bool)
         self.kv_tiles = int(np.maximum(self.tiles_q0, self.tiles_q1).sum()) if self.n_work else 0
         self.mma_tiles = int((self.tiles_q0 + self.tiles_q1).sum()) if self.n_work else 0
         # work items first: the kernel reads them as int4 (16-byte aligned)

@@ -65,3 +65,7 @@ def test_attn_plan_host_logic():
     need = lambda t: (32 * t + 31) // 128 + 1 if 32 * t < 544 else 0
     assert got == [(p, need(2 * p), need(2 * p + 1)) for p in range(9)]
     assert np.all(np.bincount(w[r1, 6]) == 9)
+    # half flags: Q tile t's last key slot 32t+31 lies in the first 64 of its last KV tile
+    for p, h0, h1 in zip(w[r1, 5], plan.half_q0[r1], plan.half_q1[r1]):
+        assert h0 == ((64 * p + 31) % 128 < 64)
+        assert h1 == (((64 * p + 63) % 128 < 64) if 64 * p + 32 < 544 else False)

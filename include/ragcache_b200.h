@@ -127,6 +127,16 @@ int rcb_kv_write_rope(const void* q, int64_t q_stride, const void* k, const void
                       void* kv_pool, int32_t block_tokens, int32_t n_layers, int32_t n_kv_heads,
                       int32_t head_dim, int32_t layer, float rope_theta, void* stream);
 
+/* Same as rcb_kv_write_rope with cos/sin read from an rcb_rope_table (identical values; no
+ * per-token sincosf): the batched serving path, 8 tokens per CTA.  rope_table_dev must cover
+ * every position. */
+int rcb_kv_write_rope_table(const void* q, int64_t q_stride, const void* k, const void* v,
+                            int64_t kv_stride, void* q_out, const int32_t* positions_dev,
+                            const int32_t* slots_dev, int32_t n_tokens, int32_t n_q_heads,
+                            void* kv_pool, int32_t block_tokens, int32_t n_layers,
+                            int32_t n_kv_heads, int32_t head_dim, int32_t layer,
+                            const void* rope_table_dev, void* stream);
+
 /* cos/sin table for fused RoPE: float2 [max_pos][head_dim/2] = (cos, sin)(pos * theta^(-2i/d)) */
 int rcb_rope_table(void* table_dev, int32_t max_pos, int32_t head_dim, float rope_theta,
                    void* stream);
@@ -142,7 +152,9 @@ int rcb_rope_table(void* table_dev, int32_t max_pos, int32_t head_dim, float rop
  *   req_meta_dev: int32 [n_req][5] = {q_start, q_len(beta), q_pos0(alpha), blk_begin, blk_count}
  *   blk_*_dev   : int32 per block-table entry: pool block id, valid tokens, logical start pos
  *   work_dev    : int32 [n_work][8] = {q_start, q_len, q_pos0, blk_begin, blk_count,
- *                 q_tile, kv_head, n_kv_tiles} (built by rcb_attn_plan, heaviest first) */
+ *                 q_pair, kv_head, n0 | half0 << 15 | n1 << 16 | half1 << 31}: two adjacent
+ *                 128-row query tiles per item and the KV tiles each needs (built by
+ *                 rcb_attn_plan, heaviest first) */
 int rcb_prefix_prefill(const void* q, int64_t q_row_stride, void* o, int32_t total_q_tokens,
                        int32_t n_q_heads, const void* kv_pool, int64_t num_pool_blocks,
                        int32_t block_tokens, int32_t n_layers, int32_t n_kv_heads,

@@ -76,6 +76,10 @@ SIGNATURES = [
     ("rcb_kv_write_rope", c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_void_p,
                                   c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_int32,
                                   c_int32, c_int32, c_int32, c_int32, c_float, c_void_p]),
+    ("rcb_kv_write_rope_table", c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_int64,
+                                        c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p,
+                                        c_int32, c_int32, c_int32, c_int32, c_int32, c_void_p,
+                                        c_void_p]),
     ("rcb_rope_table", c_int, [c_void_p, c_int32, c_int32, c_float, c_void_p]),
     ("rcb_prefix_prefill", c_int, [c_void_p, c_int64, c_void_p, c_int32, c_int32, c_void_p,
                                    c_int64, c_int32, c_int32, c_int32, c_int32, c_int32,

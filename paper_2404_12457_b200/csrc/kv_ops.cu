@@ -183,6 +183,93 @@ __global__ void __launch_bounds__(kRopeThreads)
   }
 }
 
+// Table-driven variant: cos/sin come from the rcb_rope_table (the same table the attention
+// kernel rotates Q with, computed with the same formula), so no per-token sincosf and no
+// __syncthreads; kKvTok tokens per CTA, consecutive threads take consecutive 16 B chunks
+// of a token's heads (coalesced reads of the QKV row, 256 B runs into each pool slot).
+#ifndef RCB_KV_TOK
+#define RCB_KV_TOK 8
+#endif
+#ifndef RCB_KV_UNROLL
+#define RCB_KV_UNROLL 1
+#endif
+constexpr int kKvTok = RCB_KV_TOK;
+constexpr int kKvUnroll = RCB_KV_UNROLL;
+constexpr int kKvTabThreads = 256;
+
+__global__ void __launch_bounds__(kKvTabThreads)
+    kv_write_rope_tab_kernel(const __nv_bfloat16* __restrict__ q, int64_t q_stride,
+                             const __nv_bfloat16* __restrict__ k,
+                             const __nv_bfloat16* __restrict__ v, int64_t kv_stride,
+                             __nv_bfloat16* __restrict__ q_out,
+                             const int32_t* __restrict__ positions,
+                             const int32_t* __restrict__ slots, int n_tokens, int n_q_heads,
+                             __nv_bfloat16* __restrict__ pool, int block_tokens,
+                             int64_t block_elems, int n_kv_heads, int head_dim, int layer,
+                             const float4* __restrict__ table) {
+  const int half = head_dim / 2;
+  const int cph = half / 8;  // 16-byte chunks per half row
+  const int q_heads = q != nullptr ? n_q_heads : 0;
+  const int rot_units = (q_heads + n_kv_heads) * cph;
+  const int per_tok = rot_units + n_kv_heads * (head_dim / 8);
+  const int t0 = blockIdx.x * kKvTok;
+  const int n = min(kKvTok, n_tokens - t0) * per_tok;
+  const int64_t tile = int64_t(block_tokens) * head_dim;
+#pragma unroll kKvUnroll
+  for (int u = threadIdx.x; u < n; u += kKvTabThreads) {
+    const int tt = u / per_tok;
+    const int j = u - tt * per_tok;
+    const int t = t0 + tt;
+    const int slot = __ldg(slots + t);
+    const int blk = slot / block_tokens;
+    const int off = slot - blk * block_tokens;
+    __nv_bfloat16* kbase = pool + int64_t(blk) * block_elems +
+                           int64_t(2 * layer) * n_kv_heads * tile + int64_t(off) * head_dim;
+    if (j < rot_units) {
+      const int h = j / cph;
+      const int c = (j - h * cph) * 8;
+      const __nv_bfloat16* src;
+      __nv_bfloat16* dst;
+      if (h < q_heads) {
+        src = q + int64_t(t) * q_stride + int64_t(h) * head_dim;
+        dst = q_out + (int64_t(t) * n_q_heads + h) * head_dim;
+      } else {
+        src = k + int64_t(t) * kv_stride + int64_t(h - q_heads) * head_dim;
+        dst = kbase + int64_t(h - q_heads) * tile;
+      }
+      const uint4 a = *reinterpret_cast<const uint4*>(src + c);
+      const uint4 b = *reinterpret_cast<const uint4*>(src + c + half);
+      // table row of this position: (cos, sin) of frequencies c .. c+7 = 4 float4
+      const float4* tab = table + (int64_t(__ldg(positions + t)) * half + c) / 2;
+      float cs[8], sn[8];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float4 f = __ldg(tab + e);
+        cs[2 * e] = f.x;
+        sn[2 * e] = f.y;
+        cs[2 * e + 1] = f.z;
+        sn[2 * e + 1] = f.w;
+      }
+      float x0[8], x1[8], y0[8], y1[8];
+      unpack8(a, x0);
+      unpack8(b, x1);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        y0[e] = x0[e] * cs[e] - x1[e] * sn[e];
+        y1[e] = x1[e] * cs[e] + x0[e] * sn[e];
+      }
+      *reinterpret_cast<uint4*>(dst + c) = pack8(y0);
+      *reinterpret_cast<uint4*>(dst + c + half) = pack8(y1);
+    } else {
+      const int jj = j - rot_units;
+      const int h = jj / (head_dim / 8);
+      const int c = (jj - h * (head_dim / 8)) * 8;
+      *reinterpret_cast<uint4*>(kbase + int64_t(n_kv_heads + h) * tile + c) =
+          *reinterpret_cast<const uint4*>(v + int64_t(t) * kv_stride + int64_t(h) * head_dim + c);
+    }
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_block_copy_params(const void* src_base, void* dst_base, int64_t block_bytes,
@@ -245,6 +332,32 @@ extern "C" int rcb_rope_table(void* table_dev, int32_t max_pos, int32_t head_dim
       static_cast<float2*>(table_dev), max_pos, half, head_dim, log2f(rope_theta));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return rcb::set_cuda_error(e, "rcb_rope_table");
+  return RCB_OK;
+}
+
+extern "C" int rcb_kv_write_rope_table(const void* q, int64_t q_stride, const void* k,
+                                       const void* v, int64_t kv_stride, void* q_out,
+                                       const int32_t* positions_dev, const int32_t* slots_dev,
+                                       int32_t n_tokens, int32_t n_q_heads, void* kv_pool,
+                                       int32_t block_tokens, int32_t n_layers,
+                                       int32_t n_kv_heads, int32_t head_dim, int32_t layer,
+                                       const void* rope_table_dev, void* stream) {
+  if (n_tokens == 0) return RCB_OK;
+  if (head_dim % 16 != 0 || head_dim > 256 || layer < 0 || layer >= n_layers)
+    return rcb::set_error(RCB_ERR_ARG, "head_dim must be a multiple of 16 (<= 256), layer in range");
+  if (q_stride % 8 != 0 || kv_stride % 8 != 0)
+    return rcb::set_error(RCB_ERR_ARG, "q/kv row strides must be multiples of 8 elements");
+  if (rope_table_dev == nullptr) return rcb::set_error(RCB_ERR_ARG, "rope table required");
+  const int64_t block_elems = int64_t(n_layers) * 2 * n_kv_heads * block_tokens * head_dim;
+  const int grid = (n_tokens + rcb::kKvTok - 1) / rcb::kKvTok;
+  rcb::kv_write_rope_tab_kernel<<<grid, rcb::kKvTabThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(q), q_stride, static_cast<const __nv_bfloat16*>(k),
+      static_cast<const __nv_bfloat16*>(v), kv_stride, static_cast<__nv_bfloat16*>(q_out),
+      positions_dev, slots_dev, n_tokens, n_q_heads, static_cast<__nv_bfloat16*>(kv_pool),
+      block_tokens, block_elems, n_kv_heads, head_dim, layer,
+      static_cast<const float4*>(rope_table_dev));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return rcb::set_cuda_error(e, "rcb_kv_write_rope_table");
   return RCB_OK;
 }
 

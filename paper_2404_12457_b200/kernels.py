@@ -57,15 +57,29 @@ def rope_table(max_pos: int, head_dim: int, rope_theta: float, device="cuda",
 def kv_write_rope(q, k: torch.Tensor, v: torch.Tensor, q_out, positions: torch.Tensor,
                   slots: torch.Tensor, pool_base: int, *, block_tokens: int, n_layers: int,
                   n_kv_heads: int, head_dim: int, layer: int, rope_theta: float,
-                  n_q_heads: int | None = None, stream=None) -> None:
+                  n_q_heads: int | None = None, rope: torch.Tensor | None = None,
+                  stream=None) -> None:
     """RoPE q,k then scatter k,v into the pool (q/k/v may be strided row views).
-    q = q_out = None: K/V only (Q is rotated inside prefix_prefill)."""
+    q = q_out = None: K/V only (Q is rotated inside prefix_prefill).  With ``rope`` (an
+    rcb_rope_table covering every position) cos/sin are read from it instead of being
+    recomputed per token (identical values)."""
     n_tokens = k.shape[0]
     if n_q_heads is None:
         n_q_heads = q_out.shape[1]
     assert k.stride(-1) == 1 and v.stride(-1) == 1 and k.stride(0) == v.stride(0)
     if q is not None:
         assert q.stride(-1) == 1
+    if rope is not None:  # cos/sin from an rcb_rope_table (covering every position)
+        if rope.dtype != torch.float32 or rope.shape[1] * 2 != head_dim:
+            raise ValueError(f"rope table {tuple(rope.shape)} does not match head_dim {head_dim}")
+        check(load().rcb_kv_write_rope_table(
+            _dev_ptr(q) if q is not None else None, q.stride(0) if q is not None else 0,
+            _dev_ptr(k), _dev_ptr(v), k.stride(0),
+            _dev_ptr(q_out) if q_out is not None else None,
+            _dev_ptr(positions), _dev_ptr(slots), n_tokens, n_q_heads, pool_base, block_tokens,
+            n_layers, n_kv_heads, head_dim, layer, _dev_ptr(rope), _stream(stream)),
+            "rcb_kv_write_rope_table")
+        return
     check(load().rcb_kv_write_rope(
         _dev_ptr(q) if q is not None else None, q.stride(0) if q is not None else 0,
         _dev_ptr(k), _dev_ptr(v), k.stride(0),

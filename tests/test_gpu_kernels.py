@@ -250,3 +250,33 @@ def test_prefix_prefill_fused_rope_matches_oracle(hd, hq, hkv, bt):
     pc = pool2.cpu()
     for t in (0, T // 2, T - 1):
         assert (pc[t // bt, 0, 0, :, t % bt, :].float() - k_ref[t]).abs().max().item() < 0.05
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("with_q", [True, False])
+def test_kv_write_rope_table_is_bit_identical(with_q):
+    """rcb_kv_write_rope_table (cos/sin from rcb_rope_table, 8 tokens per CTA) writes the
+    same bytes as the per-token sincosf kernel: both use theta^(-2i/d) via exp2f + sincosf."""
+    hd, hq, hkv, bt, L, nb, T, theta = 128, 32, 8, 64, 2, 96, 203, 1e6
+    g = torch.Generator(device="cuda")
+    g.manual_seed(3)
+    qkv = torch.randn((T, (hq + 2 * hkv) * hd), generator=g, device="cuda").to(torch.bfloat16)
+    q = qkv[:, : hq * hd] if with_q else None
+    k = qkv[:, hq * hd:(hq + hkv) * hd]
+    v = qkv[:, (hq + hkv) * hd:]
+    pos = (torch.randperm(5000, device="cuda")[:T] + 17).to(torch.int32)
+    slots = torch.randperm(nb * bt, device="cuda")[:T].to(torch.int32)
+    table = kernels.rope_table(int(pos.max()) + 1, hd, theta)
+    outs = []
+    for rope in (None, table):
+        pool = torch.zeros((nb, L, 2, hkv, bt, hd), dtype=torch.bfloat16, device="cuda")
+        q_out = torch.zeros((T, hq, hd), dtype=torch.bfloat16, device="cuda") if with_q else None
+        kernels.kv_write_rope(q, k, v, q_out, pos, slots, pool.data_ptr(), block_tokens=bt,
+                              n_layers=L, n_kv_heads=hkv, head_dim=hd, layer=1, rope_theta=theta,
+                              n_q_heads=hq, rope=rope)
+        torch.cuda.synchronize()
+        outs.append((pool, q_out))
+    assert torch.equal(outs[0][0].view(torch.int16), outs[1][0].view(torch.int16))
+    if with_q:
+        assert torch.equal(outs[0][1].view(torch.int16), outs[1][1].view(torch.int16))
+    assert int((outs[1][0][:, 0] != 0).sum()) == 0  # layer 0 untouched

@@ -207,10 +207,13 @@ def bench_attn():
         k = x[:, hq * hd:(hq + hkv) * hd]
         v = x[:, (hq + hkv) * hd:]
         qr = torch.empty((T, hq, hd), dtype=torch.bfloat16, device="cuda")
-        for mode, qq, qo in (("qkv", x[:, : hq * hd], qr), ("kv_only", None, None)):
+        for mode, qq, qo, tab in (("qkv", x[:, : hq * hd], qr, None),
+                                  ("kv_only", None, None, None),
+                                  ("kv_only_table", None, None, rope)):
             fn = lambda: kernels.kv_write_rope(qq, k, v, qo, pos_t, slots, pool.data_ptr(),
                                                block_tokens=bt, n_layers=L, n_kv_heads=hkv,
-                                               head_dim=hd, layer=1, rope_theta=1e6, n_q_heads=hq)
+                                               head_dim=hd, layer=1, rope_theta=1e6, n_q_heads=hq,
+                                               rope=tab)
             med, best = timed(fn)
             nbytes = T * hd * 2 * (2 * hkv * 2 + (2 * hq if qq is not None else 0))
             emit(kind="kv_write_rope", mode=mode, case=name, ms=med, gbs=nbytes / med / 1e6)

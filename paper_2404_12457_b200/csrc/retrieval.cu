@@ -103,6 +103,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                      float* __restrict__ scores_out, int n_queries) {
   using Lay = Layout<NQ>;
   constexpr int kParts = Lay::kParts;
+  // the merge kernel (launched with programmatic stream serialization) may start launching
+  // now; it waits in griddepcontrol.wait until this grid has completed
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -221,7 +224,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int p = 1; p < kParts; ++p)
 #pragma unroll
           for (int i = 0; i < KL; ++i) list_push<KL>(ls, li_, ms[(p * NQ + q) * KL + i], mi[(p * NQ + q) * KL + i]);
-        const long long base = (((long long)sg * gridDim.x + blockIdx.x) * NQ + q) * k;
+        // workspace [segment][query][CTA][k]: the merge warp of (segment, query) reads its
+        // grid x k candidates contiguously
+        const long long base = (((long long)sg * NQ + q) * gridDim.x + blockIdx.x) * k;
 #pragma unroll
         for (int i = 0; i < KL; ++i)
           if (i < k) {
@@ -316,6 +321,7 @@ __global__ void topk_merge_kernel(const float* __restrict__ part_score,
   __shared__ int seg_i[kMaxSeg][kKL];
   __shared__ float out_s[kMaxSeg][kKL];
   __shared__ int out_i[kMaxSeg][kKL];
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the scan grid completed
   const int q = blockIdx.x;
   const int s = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -324,10 +330,19 @@ __global__ void topk_merge_kernel(const float* __restrict__ part_score,
 #pragma unroll
   for (int i = 0; i < kKL; ++i) { ls[i] = -INFINITY; li[i] = INT_MAX; }
   const int n_cand = n_parts * k;
-  for (int c = lane; c < n_cand; c += 32) {
-    const int p = c / k, e = c % k;
-    const long long idx = (((long long)s * n_parts + p) * NQ + q) * k + e;
-    list_push<kKL>(ls, li, part_score[idx], part_id[idx]);
+  const long long base = ((long long)s * NQ + q) * n_cand;  // [segment][query][CTA][k]
+  // coalesced, 8 loads in flight per lane before the list updates
+  for (int c0 = 0; c0 < n_cand; c0 += 32 * 8) {
+    float cs[8];
+    int ci[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int c = c0 + u * 32 + lane;
+      cs[u] = c < n_cand ? __ldg(part_score + base + c) : -INFINITY;
+      ci[u] = c < n_cand ? __ldg(part_id + base + c) : INT_MAX;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) list_push<kKL>(ls, li, cs[u], ci[u]);
   }
   warp_topk_emit<kKL>(ls, li, k, seg_s[s], seg_i[s]);
   __syncthreads();
@@ -531,10 +546,21 @@ extern "C" int rcb_retrieval_topk(const void* corpus_dev, int64_t n_rows, int32_
   rc = ret::scan(corpus_dev, n_rows, dim, queries_dev, n_queries, n_stages, k, ps, pi, nullptr,
                  grid, st);
   if (rc != RCB_OK) return rc;
-  ret::topk_merge_kernel<<<n_queries, 32 * n_stages, 0, st>>>(
-      ps, pi, grid, nq, n_stages, k, id_offset, reinterpret_cast<long long*>(ids_out_dev),
-      scores_out_dev);
-  cudaError_t e = cudaGetLastError();
+  // programmatic dependent launch: the merge's launch overlaps the scan's tail
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_queries);
+  cfg.blockDim = dim3(32 * n_stages);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, ret::topk_merge_kernel, static_cast<const float*>(ps),
+                                     static_cast<const int*>(pi), grid, nq, n_stages, k,
+                                     static_cast<long long>(id_offset),
+                                     reinterpret_cast<long long*>(ids_out_dev), scores_out_dev);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "retrieval merge launch");
   return RCB_OK;
 }

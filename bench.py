@@ -451,7 +451,7 @@ def measure_ttft(w, swap, stage_ms: float) -> dict:
     """p50 TTFT on B200 costs: measure T(alpha, beta) of the real prefill (our kernels +
     cuBLAS GEMMs, CUDA-graph replay), then run the reference engine (ragsim, decisions
     unchanged) on this workload and on its repeated-question variant across GPU tiers."""
-    from paper_2404_12457_b200.profile import measure_profile
+    from paper_2404_12457_b200.profile import decode_ms_per_token, measure_profile
     from paper_2404_12457_b200.ttft import ttft_curve
     from paper_2404_12457_b200.workloads import WORKLOADS
 
@@ -459,21 +459,28 @@ def measure_ttft(w, swap, stage_ms: float) -> dict:
     prof, info = measure_profile(w.shape, block_tokens=w.block_tokens, reps=3)
     t_prof = time.perf_counter() - t0
     pcie = swap["h2d_gbs"] if swap else 55.0
+    # decode step cost at the workload's typical context (k docs + prompt)
+    ctx = w.k * int(w.doc_tokens_mean) + w.prompt_tokens
+    decode_ms = decode_ms_per_token(prof, ctx)
     own = ttft_curve(w, prof, gpu_tiers=[w.gpu_capacity_tokens], host_tier=w.host_capacity_tokens,
-                     n_requests=2000, pcie_gbs=pcie, stage_interval_ms=stage_ms)[0]
+                     n_requests=2000, pcie_gbs=pcie, stage_interval_ms=stage_ms,
+                     decode_ms_per_token=decode_ms)[0]
     qw = WORKLOADS.get(w.name + "-qpool")
     curve = []
     if qw is not None:
         floor = qw.k * int(qw.doc_tokens_mean) + qw.prompt_tokens + 64
         tiers = sorted({max(floor, int(x * qw.gpu_capacity_tokens)) for x in (0.002, 0.05, 0.2, 1.0)})
         curve = ttft_curve(qw, prof, gpu_tiers=tiers, host_tier=qw.host_capacity_tokens,
-                           n_requests=2000, pcie_gbs=pcie, stage_interval_ms=stage_ms)
+                           n_requests=2000, pcie_gbs=pcie, stage_interval_ms=stage_ms,
+                           decode_ms_per_token=decode_ms)
     idx = {(a, b): prof.times[i][j] for i, a in enumerate(prof.alpha_grid)
            for j, b in enumerate(prof.beta_grid)}
     return {"p50_ttft_ms": own["p50_ttft_ms"], "mean_ttft_ms": own["mean_ttft_ms"],
             "doc_hit_rate": own["doc_hit_rate"], "engine": "ragsim SimulationEngine (TieredEngine) "
-            "on the B200-measured prefill profile, rate 2 req/s, 2000 requests",
+            "on the B200-measured prefill profile and decode step, rate 2 req/s, 2000 requests",
             "retrieval_stage_ms": round(stage_ms, 4),
+            "decode_ms_per_token": {"value": round(decode_ms, 3), "context_tokens": ctx,
+                                    "replaces": "ragsim RunConfig.decode_ms_per_token = 20.0"},
             "prefill_ms": {"cached1024_new32": round(idx[(1024, 32)], 3),
                            "cached0_new1024": round(idx[(0, 1024)], 3),
                            "cached0_new4096": round(idx[(0, 4096)], 3)},

@@ -29,8 +29,18 @@ from ragsim.cost_model import DEFAULT_GRID, CostProfile  # noqa: E402
 
 # ragsim's default knots (cost_model.py:29) plus small-beta knots: a cached-prefix
 # request computes only its prompt (32 tokens), which the default grid would
-# interpolate toward T(alpha, 0) = 0
-BETA_GRID = (0, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096)
+# interpolate toward T(alpha, 0) = 0; beta = 1 is one decode step of one request
+BETA_GRID = (0, 1, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096)
+
+
+def decode_ms_per_token(profile, context_tokens: int) -> float:
+    """One decode step of one request = a one-token prefill over its cached context:
+    the model forward with the same GEMMs and the prefix-prefill kernel as the paged
+    decode attention.  Replaces ragsim's constant decode_ms_per_token (config.py:52,
+    consumed at simulator.py:419-436)."""
+    from ragsim.cost_model import interpolate
+
+    return float(interpolate(profile, context_tokens, 1))
 
 
 def measure_profile(shape: str = "mistral-7b", alpha_grid=DEFAULT_GRID, beta_grid=BETA_GRID,

@@ -27,7 +27,8 @@ from ragsim.cost_model import GIB_PER_S, save_profile_csv  # noqa: E402
 
 def ttft_curve(w: Workload, profile, *, gpu_tiers, host_tier: int, n_requests: int = 3000,
                rate: float = 2.0, pcie_gbs: float = 55.0, stage_provider_fn=None,
-               stage_interval_ms: float | None = None, seed: int = 0) -> list[dict]:
+               stage_interval_ms: float | None = None, decode_ms_per_token: float | None = None,
+               seed: int = 0) -> list[dict]:
     trace, sizes = make_stream(w, n_requests, rate=rate, seed=seed)
     with tempfile.TemporaryDirectory() as td:
         path = os.path.join(td, "b200_profile.csv")
@@ -39,7 +40,9 @@ def ttft_curve(w: Workload, profile, *, gpu_tiers, host_tier: int, n_requests: i
                             kv_bytes_per_token=float(w.model.kv_bytes_per_token),
                             pcie_bandwidth_bytes_per_ms=pcie_gbs * 1e9 / 1e3, seed=seed,
                             **({"stage_interval_ms": stage_interval_ms}
-                               if stage_interval_ms is not None else {}))
+                               if stage_interval_ms is not None else {}),
+                            **({"decode_ms_per_token": decode_ms_per_token}
+                               if decode_ms_per_token is not None else {}))
             min_doc = min(sizes.values())
             pool = accounting_pool(pool_blocks(cap, w.block_tokens, min_doc, 8 * (w.k + 1)),
                                    pool_blocks(host_tier, w.block_tokens, min_doc, 0) or 1,

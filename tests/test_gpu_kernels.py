@@ -147,6 +147,8 @@ ATTN_CASES = [
     (128, 32, 32, 64, 1, [([512], [512, 32]), ([200, 100], [5])]),
     (128, 8, 1, 32, 1, [([77], [130, 17])]),
     (64, 8, 4, 128, 1, [([129, 3], [260])]),
+    # decode steps (one new token per request over its cached context): split items
+    (128, 32, 8, 64, 1, [([512, 512], [1]), ([300], [1]), ([512, 512, 512, 512], [1])]),
 ]
 
 

@@ -158,6 +158,9 @@ def bench_attn():
         ("mistral mixed step", 32, 8, 64, [(0, 1056)] * 26 + [(512, 544)] * 26 + [(1024, 32)] * 12),
         ("llama2 miss a0 b544 x16", 32, 32, 64, [(0, 544)] * 16),
         ("mistral long a4096 b256 x32", 32, 8, 64, [(4096, 256)] * 32),
+        # a decode step: one new token per request over its cached context (HBM-bound)
+        ("mistral decode a1056 b1 x64", 32, 8, 64, [(1056, 1)] * 64),
+        ("mistral decode a4096 b1 x64", 32, 8, 64, [(4096, 1)] * 64),
     ]
     only = os.environ.get("MB_CASE")
     for name, hq, hkv, bt, reqs in cases:

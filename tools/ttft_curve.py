@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from paper_2404_12457_b200 import kernels, synth  # noqa: E402
-from paper_2404_12457_b200.profile import measure_profile  # noqa: E402
+from paper_2404_12457_b200.profile import decode_ms_per_token, measure_profile  # noqa: E402
 from paper_2404_12457_b200.retrieval import GpuStageProvider, synthetic_query_fn  # noqa: E402
 from paper_2404_12457_b200.ttft import ttft_curve  # noqa: E402
 from paper_2404_12457_b200.workloads import WORKLOADS  # noqa: E402
@@ -60,10 +60,13 @@ def main():
     floor = w.k * int(w.doc_tokens_mean) + w.prompt_tokens + 64
     tiers = sorted({max(floor, t) for t in tiers})
     t1 = time.time()
+    decode_ms = decode_ms_per_token(prof, w.k * int(w.doc_tokens_mean) + w.prompt_tokens)
     rows = ttft_curve(w, prof, gpu_tiers=tiers, host_tier=w.host_capacity_tokens,
-                      n_requests=n_req, rate=rate, stage_provider_fn=provider)
+                      n_requests=n_req, rate=rate, stage_provider_fn=provider,
+                      decode_ms_per_token=decode_ms)
     out = {"workload": name, "shape": w.shape, "profile": info, "profile_seconds": round(t_prof, 1),
-           "stage_interval_ms": round(stage_ms, 4), "rate_req_s": rate, "requests": n_req,
+           "stage_interval_ms": round(stage_ms, 4), "decode_ms_per_token": round(decode_ms, 3),
+           "rate_req_s": rate, "requests": n_req,
            "engine_seconds": round(time.time() - t1, 1),
            "profile_ms": {f"a{a}_b{b}": round(prof.times[i][j], 3)
                           for i, a in enumerate(prof.alpha_grid) for j, b in enumerate(prof.beta_grid)},

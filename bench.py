@@ -452,7 +452,7 @@ def measure_ttft(w, swap, stage_ms: float) -> dict:
     cuBLAS GEMMs, CUDA-graph replay), then run the reference engine (ragsim, decisions
     unchanged) on this workload and on its repeated-question variant across GPU tiers."""
     from paper_2404_12457_b200.profile import decode_ms_per_token, measure_profile
-    from paper_2404_12457_b200.ttft import ttft_curve
+    from paper_2404_12457_b200.ttft import slo_throughput, ttft_curve
     from paper_2404_12457_b200.workloads import WORKLOADS
 
     t0 = time.perf_counter()
@@ -466,13 +466,18 @@ def measure_ttft(w, swap, stage_ms: float) -> dict:
                      n_requests=2000, pcie_gbs=pcie, stage_interval_ms=stage_ms,
                      decode_ms_per_token=decode_ms)[0]
     qw = WORKLOADS.get(w.name + "-qpool")
-    curve = []
+    curve, slo, slo_s = [], [], 0.0
     if qw is not None:
         floor = qw.k * int(qw.doc_tokens_mean) + qw.prompt_tokens + 64
         tiers = sorted({max(floor, int(x * qw.gpu_capacity_tokens)) for x in (0.002, 0.05, 0.2, 1.0)})
         curve = ttft_curve(qw, prof, gpu_tiers=tiers, host_tier=qw.host_capacity_tokens,
                            n_requests=2000, pcie_gbs=pcie, stage_interval_ms=stage_ms,
                            decode_ms_per_token=decode_ms)
+        t1 = time.perf_counter()
+        slo = slo_throughput(qw, prof, gpu_tiers=[tiers[0], tiers[-1]],
+                             host_tier=qw.host_capacity_tokens, pcie_gbs=pcie,
+                             decode_ms_per_token=decode_ms)
+        slo_s = time.perf_counter() - t1
     idx = {(a, b): prof.times[i][j] for i, a in enumerate(prof.alpha_grid)
            for j, b in enumerate(prof.beta_grid)}
     return {"p50_ttft_ms": own["p50_ttft_ms"], "mean_ttft_ms": own["mean_ttft_ms"],
@@ -485,6 +490,11 @@ def measure_ttft(w, swap, stage_ms: float) -> dict:
                            "cached0_new1024": round(idx[(0, 1024)], 3),
                            "cached0_new4096": round(idx[(0, 4096)], 3)},
             "profile": info, "profile_seconds": round(t_prof, 1),
+            "req_per_s_at_5x_slo": {"workload": qw.name if qw else None,
+                                    "how": "ragsim measure_throughput (simulator.py:648-681) on "
+                                           "the B200 profile + decode step",
+                                    "points": slo if qw is not None else [],
+                                    "seconds": round(slo_s, 1) if qw is not None else None},
             "vs_hit_rate": {"workload": qw.name if qw else None,
                             "points": [{k: r[k] for k in ("gpu_tier_tokens", "doc_hit_rate",
                                                           "p50_ttft_ms", "mean_ttft_ms")}

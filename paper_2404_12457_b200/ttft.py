@@ -23,6 +23,7 @@ from .workloads import Workload, make_stream, pool_blocks
 import_ragsim()
 from ragsim.config import RunConfig  # noqa: E402
 from ragsim.cost_model import GIB_PER_S, save_profile_csv  # noqa: E402
+from ragsim.simulator import measure_throughput, run as ragsim_run  # noqa: E402
 
 
 def ttft_curve(w: Workload, profile, *, gpu_tiers, host_tier: int, n_requests: int = 3000,
@@ -56,4 +57,32 @@ def ttft_curve(w: Workload, profile, *, gpu_tiers, host_tier: int, n_requests: i
                          "mean_ttft_ms": round(a["mean_ttft_ms"], 3),
                          "p99_ttft_ms": round(a["p99_ttft_ms"], 3),
                          "swap_outs": a["swap_outs"], "requests": a["requests"]})
+    return rows
+
+
+def slo_throughput(w: Workload, profile, *, gpu_tiers, host_tier: int, n_requests: int = 600,
+                   pcie_gbs: float = 55.0, decode_ms_per_token: float | None = None,
+                   slo_multiplier: float = 5.0, min_rate: float = 0.5, max_rate: float = 400.0,
+                   iterations: int = 10, seed: int = 0) -> list[dict]:
+    """RAG req/s in the paper's sense: the highest Poisson arrival rate
+    whose mean TTFT stays within 5x the light-load mean TTFT, found by the reference's own
+    bisection (measure_throughput, simulator.py:648-681) on B200-measured costs, per GPU
+    tier (-> document hit rate)."""
+    trace, sizes = make_stream(w, n_requests, rate=2.0, seed=seed)
+    rows = []
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "b200_profile.csv")
+        save_profile_csv(profile, path)
+        for cap in gpu_tiers:
+            cfg = RunConfig(gpu_capacity_tokens=cap, host_capacity_tokens=host_tier, k=w.k,
+                            profile_path=path,
+                            kv_bytes_per_token=float(w.model.kv_bytes_per_token),
+                            pcie_bandwidth_bytes_per_ms=pcie_gbs * 1e9 / 1e3, seed=seed,
+                            **({"decode_ms_per_token": decode_ms_per_token}
+                               if decode_ms_per_token is not None else {}))
+            rps = measure_throughput(cfg, trace, sizes, slo_multiplier, min_rate, max_rate,
+                                     iterations=iterations)
+            hit = ragsim_run(cfg, trace, sizes).aggregates()["doc_hit_rate"]
+            rows.append({"gpu_tier_tokens": cap, "doc_hit_rate": round(hit, 4),
+                         "req_per_s_at_slo": round(rps, 3)})
     return rows

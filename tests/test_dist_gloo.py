@@ -129,3 +129,23 @@ def test_shard_bounds_and_route_partition():
     reqs = [R(i) for i in range(37)]
     parts = [route(reqs, r, 4) for r in range(4)]
     assert sorted(x.id for p in parts for x in p) == list(range(37))
+
+
+def test_slo_throughput_rises_with_hit_rate():
+    """ragsim's measure_throughput on a profile: more GPU tier -> more doc hits -> a
+    higher arrival rate fits the 5x TTFT SLO (the paper's throughput metric)."""
+    from paper_2404_12457_b200._ragsim import ragsim_available
+
+    if not ragsim_available():
+        pytest.skip("ragsim not importable")
+    from ragsim.cost_model import synthetic_profile
+
+    from paper_2404_12457_b200.ttft import slo_throughput
+    from paper_2404_12457_b200.workloads import WORKLOADS
+
+    qw = WORKLOADS["mistral7b-100k-qpool"]
+    lo, hi = slo_throughput(qw, synthetic_profile(), gpu_tiers=[2200, qw.gpu_capacity_tokens],
+                            host_tier=qw.host_capacity_tokens, n_requests=300,
+                            decode_ms_per_token=5.0, iterations=8)
+    assert hi["doc_hit_rate"] > lo["doc_hit_rate"] + 0.3
+    assert hi["req_per_s_at_slo"] > lo["req_per_s_at_slo"]

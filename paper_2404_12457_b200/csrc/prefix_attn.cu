@@ -46,6 +46,24 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #endif
 constexpr int kPolyCols = RCB_POLY_COLS;
 
+// Per-step handoff timestamps of CTA 0 (debug builds with -DRCB_TRACE only; tools/attn_trace.py)
+//   softmax WG w, its tile c: [c][4w + 0] S wait start, [4w + 1] S seen, [4w + 2] P arrive
+//   MMA, step s: [s][8] P0 seen, [9] QK0 issued, [10] P1 seen, [11] QK1 issued,
+//   [12] K(s) seen full, [13] PV0 issued, [14] PV1 issued
+#ifdef RCB_TRACE
+constexpr int kTraceTiles = 1024;
+constexpr int kTraceEv = 16;
+__device__ long long g_trace[kTraceTiles * kTraceEv];
+#define TRACE(g, ev)                                                                      \
+  do {                                                                                    \
+    if (blockIdx.x == 0 && (g) < kTraceTiles) g_trace[(g) * kTraceEv + (ev)] = clock64(); \
+  } while (0)
+#else
+#define TRACE(g, ev) \
+  do {               \
+  } while (0)
+#endif
+
 // barrier indices (pairs indexed by item parity or by query tile w)
 enum Bar {
   kQFull0 = 0, kQEmpty0 = 2, kQReady0 = 4, kSFull0 = 6, kPFull0 = 8, kOFull0 = 10,
@@ -258,6 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc_pv = idesc_bf16_f32(128, HD, 0, 1);
       const uint32_t q_base = smem_u32(sQ);
       const uint32_t kv_base = smem_u32(sKV);
+      int s = 0;           // KV step
       int c[2] = {0, 0};   // QK_w issued so far (S_w / P_w phases)
       int oc[2] = {0, 0};  // items with a non-empty Q_w so far (O_w phases)
       // the previous step's pending PVs
@@ -273,6 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           p_v_ready = true;
         }
         mbar_wait(&bar[kPFull0 + w], p_c[w] & 1);
+        TRACE(s - 1, 8 + 2 * w);
         tc_fence_after();
         const int st = p_vu % NS;
         const int nkk = p_half[w] ? kKeys / 32 : kKeys / 16;  // a half tile: 64 keys
@@ -289,6 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           umma_commit(&bar[kOFull0 + w]);
           ++oc[w];
         }
+        TRACE(s - 1, 13 + w);
       };
       auto issue_qk = [&](int w, int qt, int ku, bool half) {  // qt: Q buffer [parity][tile]
         const int st = ku % NS;
@@ -303,7 +324,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit(&bar[kSFull0 + w]);
         ++c[w];
       };
-      int s = 0;
       for (int idx = blockIdx.x, ii = 0; idx < n_work; idx += gridDim.x, ++ii) {
         const Item it = load_item(work, idx);
         const int n = it.n();
@@ -317,6 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (j == 0)  // Q landed (and, with fused RoPE, rotated by the epilogue WG)
             mbar_wait(&bar[(rope != nullptr ? kQReady0 : kQFull0) + qb], (ii >> 1) & 1);
             mbar_wait(&kv_full[ku % NS], (ku / NS) & 1);
+            TRACE(s, 12);
             tc_fence_after();
             k_ready = true;
           };
@@ -327,6 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (h0) {
             need_k();
             issue_qk(0, qb * 2, ku, it.half(0, j));
+            TRACE(s, 9);
           }
           if (p_has[1]) issue_pv(1);
           if (p_any) umma_commit(&kv_empty[p_vu % NS]);  // V(s-1) no longer read
@@ -334,6 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (h1) {
             need_k();
             issue_qk(1, qb * 2 + it.qtile(1), ku, it.half(1, j));
+            TRACE(s, 11);
           }
           umma_commit(&kv_empty[ku % NS]);  // K(s) no longer read
           if (j == n - 1) umma_commit(&bar[kQEmpty0 + qb]);  // Q tiles no longer read
@@ -398,7 +421,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!it.on(wg, j)) continue;
         // S-full also means this WG's previous PV retired (issued before QK_w(j)): O_w is
         // current
+        const bool tr = (threadIdx.x & 127) == 0 && quad == 0;
+        if (tr) TRACE(c, 4 * wg + 0);
         mbar_wait(&bar[kSFull0 + wg], c & 1);
+        if (tr) TRACE(c, 4 * wg + 1);
         tc_fence_after();
         const bool masked = !all_valid || max_pos > qp;
         const bool half = it.half(wg, j);  // only S columns [0, 64) were computed
@@ -501,6 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&bar[kPFull0 + wg]);
+        if (tr) TRACE(c, 4 * wg + 2);
         ++c;
       }
       if (it.has(wg)) {

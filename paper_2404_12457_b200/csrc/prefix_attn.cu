@@ -65,10 +65,14 @@ __device__ long long g_trace[kTraceTiles * kTraceEv];
 #endif
 
 // barrier indices (pairs indexed by item parity or by query tile w)
+// P handoff per 64-key half: kPFull0 = P columns of keys [0, 64), kPFullB0 = keys [64, 128)
+// (arrived for every tile, right after kPFull0 on a half tile); kPVDone0 = PV of the first
+// half retired (waited only by a softmax that must rescale O between its two halves)
 enum Bar {
   kQFull0 = 0, kQEmpty0 = 2, kQReady0 = 4, kSFull0 = 6, kPFull0 = 8, kOFull0 = 10,
   kOFree0 = 12, kLFull0 = 14, kLFree0 = 16, kMetaFull0 = 18, kMetaFree0 = 22,
-  kKVFull0 = 26  // [kStages] full, then [kStages] empty
+  kPFullB0 = 26, kPVDone0 = 28,
+  kKVFull0 = 30  // [kStages] full, then [kStages] empty
 };
 
 template <int HD, int BT>
@@ -170,6 +174,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar[kQReady0 + b], kRows);
       mbar_init(&bar[kSFull0 + b], 1);
       mbar_init(&bar[kPFull0 + b], kRows);
+      mbar_init(&bar[kPFullB0 + b], kRows);
+      mbar_init(&bar[kPVDone0 + b], 1);
       mbar_init(&bar[kOFull0 + b], 1);
       mbar_init(&bar[kOFree0 + b], kRows);
       mbar_init(&bar[kLFull0 + b], kRows);
@@ -291,19 +297,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&kv_full[p_vu % NS], (p_vu / NS) & 1);
           p_v_ready = true;
         }
+        // keys [0, 64): their P is packed while the softmax still works on keys [64, 128)
         mbar_wait(&bar[kPFull0 + w], p_c[w] & 1);
         TRACE(s - 1, 8 + 2 * w);
         tc_fence_after();
         const int st = p_vu % NS;
-        const int nkk = p_half[w] ? kKeys / 32 : kKeys / 16;  // a half tile: 64 keys
+        // A = P_w (bf16 pairs over S_w's first 64 columns); V tile is [half][128 keys][64]:
+        // MN-major, halves 16 KB apart (LBO)
 #pragma unroll
-        for (int kk = 0; kk < kKeys / 16; ++kk) {
-          if (kk >= nkk) break;
-          // A = P_w (bf16 pairs over S_w's first 64 columns); V tile is [half][128 keys][64]:
-          // MN-major, halves 16 KB apart (LBO)
+        for (int kk = 0; kk < kKeys / 32; ++kk) {
           const uint64_t b = sw128_desc(kv_base + st * S::kKV + kk * 2048, 16384, 1024);
           umma_bf16_ts(tmem + 256 + w * 128, tmem + w * kKeys + kk * 8, b, idesc_pv,
                        (!p_first[w] || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(&bar[kPVDone0 + w]);
+        if (!p_half[w]) {  // keys [64, 128)
+          mbar_wait(&bar[kPFullB0 + w], p_c[w] & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = kKeys / 32; kk < kKeys / 16; ++kk) {
+            const uint64_t b = sw128_desc(kv_base + st * S::kKV + kk * 2048, 16384, 1024);
+            umma_bf16_ts(tmem + 256 + w * 128, tmem + w * kKeys + kk * 8, b, idesc_pv, 1u);
+          }
         }
         if (p_last[w]) {
           umma_commit(&bar[kOFull0 + w]);
@@ -428,10 +443,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const bool masked = !all_valid || max_pos > qp;
         const bool half = it.half(wg, j);  // only S columns [0, 64) were computed
-        // Two 64-column chunks against the running max m (within 2^8 of the true row max:
-        // a chunk that exceeds m + 2^8 rescales O, l and the already-packed P of chunk 0).
-        // P of chunk c (bf16 pairs) goes to S columns [32c, 32c + 32): chunk 0's own
-        // columns, then chunk 0's (already consumed) columns for chunk 1.
+        // Two 64-column chunks against the running max m (within 2^8 of the true row max: a
+        // chunk that exceeds m + 2^8 rescales O and l).  P of chunk c (bf16 pairs) goes to S
+        // columns [32c, 32c + 32) and is handed to the MMA warp per chunk, so the PV of keys
+        // [0, 64) runs on the tensor core while chunk 1 is still being computed.
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
           if (ch == 1 && half) break;
@@ -472,7 +487,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             rescale = true;
           }
           if (__any_sync(0xffffffffu, rescale)) {
-            if (j > it.first(wg)) {  // O_w holds PV_w of this item's earlier tiles, all retired
+            // chunk 0: O_w holds PV_w of this item's earlier tiles (all retired).  chunk 1:
+            // chunk 0's P (packed against the old max) is already being consumed by the
+            // first-half PV, so let that retire and rescale O_w as a whole instead
+            if (ch == 1) {
+              mbar_wait(&bar[kPVDone0 + wg], c & 1);
+              tc_fence_after();
+            }
+            if (ch == 1 || j > it.first(wg)) {
 #pragma unroll
               for (int cc = 0; cc < HD / 32; ++cc) {
                 uint32_t r[32];
@@ -482,17 +504,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
                 tmem_st32(o_col + cc * 32, r);
               }
-            }
-            if (ch == 1) {  // chunk 0's P was packed against the old m
-              uint32_t r[32];
-              tmem_ld32(s_col, r);
-              tmem_wait_ld();
-#pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                const float2 f = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&r[i]));
-                r[i] = pack_bf16(f.x * alpha, f.y * alpha);
-              }
-              tmem_st32(s_col, r);
             }
             tmem_wait_st();
           }
@@ -523,10 +534,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < kKeys / 4; ++i) pk[i] = pack_bf16(s[2 * i], s[2 * i + 1]);
           tmem_st32(s_col + ch * (kKeys / 4), pk);
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(&bar[(ch == 0 ? kPFull0 : kPFullB0) + wg]);
         }
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(&bar[kPFull0 + wg]);
+        if (half) mbar_arrive(&bar[kPFullB0 + wg]);  // one phase per tile
         if (tr) TRACE(c, 4 * wg + 2);
         ++c;
       }

@@ -282,3 +282,45 @@ def test_kv_write_rope_table_is_bit_identical(with_q):
     if with_q:
         assert torch.equal(outs[0][1].view(torch.int16), outs[1][1].view(torch.int16))
     assert int((outs[1][0][:, 0] != 0).sum()) == 0  # layer 0 untouched
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fused_rope", [False, True])
+def test_prefix_prefill_bench_shape_sampled(fused_rope):
+    """The bench's step shape (Mistral-7B heads, 64-token blocks, 64 requests: 26 misses of
+    1056 tokens, 26 half hits 512+544, 12 full hits 1024+32 -> pair, split and half items,
+    42K query tokens) in ONE launch; one request of each kind checked against the fp32
+    oracle (the whole step is too slow for the CPU oracle)."""
+    hq, hkv, hd, bt, L, theta = 32, 8, 128, 64, 1, 1e6
+    reqs = [(0, 1056)] * 26 + [(512, 544)] * 26 + [(1024, 32)] * 12
+    n_slots = sum(-(-(a + b) // bt) for a, b in reqs)
+    nb = n_slots + 16
+    pool = _pool(nb, L, hkv, bt, hd, seed=21)
+    free = list(np.random.default_rng(5).permutation(nb))
+    requests = []
+    for a, b in reqs:
+        blocks, valid = _table([a + b], bt, free)
+        requests.append((b, a, blocks, valid))
+    T = sum(b for _, b in reqs)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(9)
+    qkv = torch.randn((T, (hq + 2 * hkv) * hd), generator=g, device="cuda").to(torch.bfloat16)
+    q = qkv[:, : hq * hd]
+    out = torch.empty((T, hq, hd), dtype=torch.bfloat16, device="cuda")
+    plan = kernels.AttnPlan(requests, block_tokens=bt, n_q_heads=hq, n_kv_heads=hkv)
+    assert (plan.tiles_q1 == 0).any() and plan.half_q0.any() and (plan.tiles_q1 > 0).any()
+    rope = kernels.rope_table(plan.max_pos + 1, hd, theta) if fused_rope else None
+    kernels.prefix_prefill(q, out, plan, pool.data_ptr(), nb, block_tokens=bt, n_layers=L,
+                           n_kv_heads=hkv, head_dim=hd, layer=0, rope=rope, n_q_heads=hq)
+    torch.cuda.synchronize()
+    pool_cpu = pool.cpu()
+    starts = np.cumsum([0] + [b for _, b in reqs])
+    for r in (0, 30, 60):  # a miss, a half hit, a full hit
+        b, a, blocks, valid = requests[r]
+        qs = q[starts[r]:starts[r] + b].cpu().float().view(b, hq, hd)
+        if fused_rope:
+            qs = attn_oracle.apply_rope(qs, a + torch.arange(b), theta)
+        ref = attn_oracle.prefix_prefill(qs, pool_cpu, [requests[r]], 0)
+        got = out[starts[r]:starts[r] + b].cpu().float()
+        err = (got - ref).abs().max().item()
+        assert err <= ATTN_ATOL, f"request {r} (alpha {a}, beta {b}): max |err| {err}"

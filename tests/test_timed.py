@@ -1,0 +1,67 @@
+"""Hardware-in-the-loop engine.
+
+CPU: with an executor that returns the profile's own interpolation, TimedEngine's
+interception of the first-chunk scheduling must reproduce ragsim.run byte for byte
+(simulator.py:481-514).  GPU: the tiny model's real prefill (GEMMs + our kernels on each
+generation's block table in the device pool, swaps included) drives the virtual clock.
+"""
+
+import pytest
+
+from paper_2404_12457_b200._ragsim import ragsim_available
+
+pytestmark = pytest.mark.skipif(not ragsim_available(), reason="ragsim not importable")
+
+
+def _desk():
+    from ragsim.config import RunConfig
+
+    from tests.golden.make_golden import DESK, desk_trace, pool_geometry
+
+    trace, sizes = desk_trace(seed=3, duration_s=200.0, rate=0.6, pool=400)
+    cfg = RunConfig(host_capacity_tokens=24576, dsp=True, stage_count=4, validate=True,
+                    prefill_chunk_ms=25.0, **DESK)
+    return cfg, trace, sizes, pool_geometry(cfg, sizes)
+
+
+def test_timed_engine_with_profile_executor_reproduces_reference():
+    from ragsim.simulator import run
+
+    from paper_2404_12457_b200.pool import accounting_pool
+    from paper_2404_12457_b200.timed import ProfileExecutor, run_timed
+
+    cfg, trace, sizes, (ng, nh) = _desk()
+    ref = run(cfg, trace, sizes)
+    rep, engine = run_timed(cfg, trace, sizes, pool=accounting_pool(ng, nh, 16),
+                            executor=ProfileExecutor())
+    assert rep.to_json(cfg) == ref.to_json(cfg)
+    assert rep.per_request_csv() == ref.per_request_csv()
+    assert len(engine.measured) >= len(trace)
+    assert all(m == p for _, _, _, p, m in engine.measured)
+
+
+@pytest.mark.gpu
+def test_timed_engine_runs_real_prefills():
+    import torch
+
+    from paper_2404_12457_b200.pool import BlockPool
+    from paper_2404_12457_b200.timed import ModelExecutor, run_timed
+
+    cfg, trace, sizes, (ng, nh) = _desk()
+    pool = BlockPool(ng, nh, block_tokens=16, n_layers=2, n_kv_heads=4, head_dim=64)
+    ex = ModelExecutor(pool, "tiny")
+    rep, engine = run_timed(cfg, trace, sizes, pool=pool, executor=ex)
+    pool.sync()
+    torch.cuda.synchronize()
+    agg = rep.aggregates()
+    assert agg["requests"] == len(trace)
+    assert len(engine.measured) >= len(trace)
+    assert all(m > 0 for *_, m in engine.measured)
+    st = pool.stats()
+    assert st["swap_out_blocks"] > 0  # the host tier was exercised with real copies
+    # a cached-prefix prefill of the same beta is no slower than computing the prefix too
+    hits = [m for _, a, b, _, m in engine.measured if a > 0 and b <= 64]
+    misses = [m for _, a, b, _, m in engine.measured if a == 0 and b > 512]
+    if hits and misses:
+        assert sorted(hits)[len(hits) // 2] < sorted(misses)[len(misses) // 2]
+    pool.close()

@@ -34,7 +34,8 @@ def main():
     prof, info = measure_profile(w.shape, block_tokens=w.block_tokens)
     t_prof = time.time() - t0
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    save_profile_csv(prof, os.path.join(ROOT, "profiles", f"{w.shape}_b200_profile.csv"))
+    save_profile_csv(prof, os.path.join(os.environ.get("OUT_DIR", os.path.join(ROOT, "profiles")),
+                                        f"{w.shape}_b200_profile.csv"))
     corpus = synth.corpus_device(w.num_docs, seed=w.seed)
     # measured per-stage scan time (64-query batch) -> stage interval
     q = torch.randint(-100, 100, (64, synth.EMB_DIM), device="cuda").to(torch.bfloat16)
@@ -74,7 +75,9 @@ def main():
     base = rows[0]["p50_ttft_ms"]
     for r in rows:
         r["p50_speedup_vs_smallest_tier"] = round(base / r["p50_ttft_ms"], 3)
-    json.dump(out, open(os.path.join(ROOT, "profiles", f"{name}_ttft_curve.json"), "w"), indent=1)
+    out_dir = os.environ.get("OUT_DIR", os.path.join(ROOT, "profiles"))  # gpurun: gpurun_out
+    os.makedirs(out_dir, exist_ok=True)
+    json.dump(out, open(os.path.join(out_dir, f"{name}_ttft_curve.json"), "w"), indent=1)
     print(json.dumps(out))
 
 

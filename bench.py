@@ -706,9 +706,10 @@ def run_reference(args, dist: Dist):
     hp = HotPath(w.model, gpu_capacity_tokens=w.gpu_capacity_tokens,
                  host_capacity_tokens=w.host_capacity_tokens, block_tokens=w.block_tokens,
                  num_gpu_blocks=ng, num_host_blocks=nh, sizes=sizes, profile=synthetic_profile(),
-                 pool=EventLog(accounting_pool(ng, nh, w.block_tokens)))
+                 pool=EventLog(accounting_pool(ng, nh, w.block_tokens)),
+                 indexed_leaves=False)  # the reference's own linear victim scan
     corpus_cpu = synth.corpus_int(w.num_docs, seed=w.seed)
-    n_req = 2
+    n_req, n_layers_sample = 4, 2
     times = []
     n_warm = args.cache_warm_steps
     from paper_2404_12457_b200.hotpath import StepPlan
@@ -720,8 +721,9 @@ def run_reference(args, dist: Dist):
         plan = StepPlan(adm, hp.pool.take(), [])
         if i >= n_warm:
             q = synth.build_queries(lambda ids: corpus_cpu[ids], [a.docs for a in adm])
-            t_ret, t_attn = cpu_step_sample(w, plan, n_req, 1, corpus_cpu, q)
-            per_req = t_dec / len(adm) + t_ret / n_req + t_attn / n_req * w.model.n_layers
+            t_ret, t_attn = cpu_step_sample(w, plan, n_req, n_layers_sample, corpus_cpu, q)
+            per_req = (t_dec / len(adm) + t_ret / n_req
+                       + t_attn / n_req / n_layers_sample * w.model.n_layers)
             times.append(per_req)
         t0 = time.perf_counter()
         for a in adm:
@@ -732,9 +734,10 @@ def run_reference(args, dist: Dist):
     timed = times[args.warmup:] or times
     per_req = sum(timed) / len(timed)
     value = 1.0 / per_req
-    sample = (f"per step: ragsim decisions for {R} requests + {n_req} requests of numpy exact "
-              f"staged top-k over {w.num_docs} docs + fp32 CPU prefix attention for 1 of "
-              f"{w.model.n_layers} layers, extrapolated per request")
+    sample = (f"per step: ragsim decisions for {R} requests (the reference tree, linear victim "
+              f"scan) + {n_req} requests of numpy exact staged top-k over {w.num_docs} docs + "
+              f"fp32 CPU prefix attention for {n_layers_sample} of {w.model.n_layers} layers, "
+              f"extrapolated per request")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "req/s",
         "n_gpus": dist.world, "steps": len(timed), "warmup": args.warmup,

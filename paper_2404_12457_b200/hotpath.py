@@ -106,7 +106,8 @@ class HotPath:
     def __init__(self, shape: ModelShape, *, gpu_capacity_tokens: int, host_capacity_tokens: int,
                  block_tokens: int, num_gpu_blocks: int, num_host_blocks: int, sizes,
                  profile, policy: str = "pgdsf", pool=None, device_pool: bool = True,
-                 swap_mode: int = RCB_SWAP_STAGED, copy_stream=None) -> None:
+                 swap_mode: int = RCB_SWAP_STAGED, copy_stream=None,
+                 indexed_leaves: bool = True) -> None:
         self.shape = shape
         self.sizes = sizes
         self.profile = profile
@@ -121,8 +122,10 @@ class HotPath:
             else:
                 pool = accounting_pool(num_gpu_blocks, num_host_blocks, block_tokens)
         self.pool = pool
+        # indexed_leaves=False keeps the reference's linear victim scan (the CPU arm)
         self.tree = TieredKnowledgeTree(gpu_capacity_tokens, host_capacity_tokens,
-                                        policy=make_policy(policy), pool=pool)
+                                        policy=make_policy(policy), pool=pool,
+                                        indexed_leaves=indexed_leaves)
         self._keys = itertools.count()
         self._rope = None  # cos/sin table for RoPE fused into the attention kernel
 

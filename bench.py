@@ -402,7 +402,6 @@ def run_ours(args, dist: Dist):
                     "bf16 embeddings, random bf16 activations in place of model projections)",
             "config": {
                 "workload": w.name,
-                "model_shape": shape.name,
                 "batch_per_gpu": R,
                 "corpus_docs": w.num_docs,
                 "doc_tokens": int(w.doc_tokens_mean),
@@ -414,6 +413,10 @@ def run_ours(args, dist: Dist):
                 "parallelism": f"dp{dist.world} (tree replicas) + corpus shards",
                 "l2": "inputs larger than L2 (corpus scan 154 MB, KV pages ~135 MB/request)",
             },
+            "kv_geometry": {"source_shape": shape.name, "n_layers": shape.n_layers,
+                            "n_q_heads": shape.n_q_heads, "n_kv_heads": shape.n_kv_heads,
+                            "head_dim": shape.head_dim,
+                            "kv_bytes_per_token": shape.kv_bytes_per_token},
             "doc_hit_rate": round(hit_rate, 4),
             "retrieval_final_stage_matches_ground_truth": retrieval_exact,
             "roofline": {
@@ -743,7 +746,7 @@ def run_reference(args, dist: Dist):
         "n_gpus": dist.world, "steps": len(timed), "warmup": args.warmup,
         "ms_per_step": round(per_req * R * 1e3, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": w.name, "model_shape": w.model.name, "batch_per_gpu": R},
+        "config": {"workload": w.name, "batch_per_gpu": R},
         "cpu_baseline": {"value": round(value, 4), "unit": "req/s", "cores": threads,
                          "kind": "port", "sample": sample},
         "e2e": {"value": round(value, 4), "unit": "req/s", "h2d_bytes_per_step": 0,

@@ -107,6 +107,19 @@ int rcb_pool_flush(rcb_pool* pool);
 int rcb_pool_fence_into(rcb_pool* pool, void* stream);
 int rcb_pool_wait_for(rcb_pool* pool, void* stream);
 int rcb_pool_sync(rcb_pool* pool);
+/* layer-pipelined swap-in (replaces the serial charge
+ * `transfer_ms + prefill_ms` of _admit, simulator.py:505-510, with overlap):
+ * issue the pending H2D batch as groups of `layers_per_group` layers (one
+ * strided DMA per block run and group, one event per group).  A pending D2H
+ * batch is issued as by rcb_pool_flush. */
+int rcb_pool_flush_layered(rcb_pool* pool, int32_t layers_per_group);
+/* make `stream` wait only for the layer group holding `layer` of the last
+ * layered batch (full rcb_pool_fence_into when none is outstanding) */
+int rcb_pool_fence_layer(rcb_pool* pool, int32_t layer, void* stream);
+/* block until the copies already issued on the copy stream, and a pending
+ * swap-out batch, finish (a pending swap-in batch stays pending): swap-outs, which the reference keeps off the critical
+ * path (simulator.py:505-507), are drained before a measured prefill */
+int rcb_pool_drain(rcb_pool* pool);
 
 /* ------------------------------------------------------------------ kernels */
 

@@ -72,6 +72,9 @@ SIGNATURES = [
     ("rcb_pool_fence_into", c_int, [c_void_p, c_void_p]),
     ("rcb_pool_wait_for", c_int, [c_void_p, c_void_p]),
     ("rcb_pool_sync", c_int, [c_void_p]),
+    ("rcb_pool_flush_layered", c_int, [c_void_p, c_int32]),
+    ("rcb_pool_fence_layer", c_int, [c_void_p, c_int32, c_void_p]),
+    ("rcb_pool_drain", c_int, [c_void_p]),
     ("rcb_kv_block_copy", c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_int32, c_void_p]),
     ("rcb_kv_write_rope", c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_void_p,
                                   c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_int32,

@@ -88,6 +88,10 @@ struct rcb_pool {
   // inside a batch would otherwise race in the zero-copy kernel)
   std::unordered_set<int32_t> pend_gpu, pend_host;
   int64_t stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  // layer-pipelined swap-in (rcb_pool_flush_layered): one event per layer group
+  // of the last layered H2D batch; invalidated by any later copy issue
+  std::vector<cudaEvent_t> ev_layer;
+  int32_t layered_groups = 0, group_layers = 0;
 
   int32_t nblocks(int32_t tokens) const { return (tokens + bt - 1) / bt; }
 };
@@ -160,6 +164,7 @@ int flush(rcb_pool* p) {
   const bool to_host = p->pending_dir == 1;
   auto& pr = p->pending;
   int rc = RCB_OK;
+  p->layered_groups = 0;  // later copies are not covered by the per-layer events
   if (p->swap_mode == RCB_SWAP_ZEROCOPY) {
     for (size_t lo = 0; lo < pr.size() && rc == RCB_OK; lo += rcb::kPairsPerLaunch) {
       const size_t hi = std::min(pr.size(), lo + rcb::kPairsPerLaunch);
@@ -223,6 +228,54 @@ int enqueue(rcb_pool* p, int dir, const std::vector<int32_t>& g, const std::vect
     p->pend_gpu.insert(g[i]);
     p->pend_host.insert(h[i]);
   }
+  return RCB_OK;
+}
+
+// Layer-pipelined swap-in: the pending H2D batch is issued as G
+// groups of `lpg` layers.  Within a block the layer slices are contiguous
+// ([L][2][H_kv][B][d_h]), so group g of a run of consecutive (gpu, host) block
+// pairs is ONE strided DMA (cudaMemcpy2DAsync: width = lpg layer slices, pitch =
+// block_bytes, height = run length).  Event g is recorded after group g; the
+// prefill's attention for layer l waits only for its group (rcb_pool_fence_layer).
+int flush_layered_h2d(rcb_pool* p, int32_t lpg) {
+  const int32_t groups = (p->layers + lpg - 1) / lpg;
+  while (static_cast<int32_t>(p->ev_layer.size()) < groups) {
+    cudaEvent_t ev;
+    cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return set_cuda_error(e, "pool layer event");
+    p->ev_layer.push_back(ev);
+  }
+  auto& pr = p->pending;
+  std::vector<std::pair<size_t, size_t>> runs;  // [i, j) with consecutive gpu and host blocks
+  for (size_t i = 0; i < pr.size();) {
+    size_t j = i + 1;
+    while (j < pr.size() && pr[j].first == pr[j - 1].first + 1 && pr[j].second == pr[j - 1].second + 1)
+      ++j;
+    runs.emplace_back(i, j);
+    i = j;
+  }
+  const int64_t layer_bytes = p->block_bytes / p->layers;
+  for (int32_t g = 0; g < groups; ++g) {
+    const int32_t l0 = g * lpg, l1 = std::min(p->layers, l0 + lpg);
+    const int64_t off = int64_t(l0) * layer_bytes, width = int64_t(l1 - l0) * layer_bytes;
+    for (const auto& r : runs) {
+      uint8_t* dst = p->gpu_base + int64_t(pr[r.first].first) * p->block_bytes + off;
+      const uint8_t* src = p->host_base + int64_t(pr[r.first].second) * p->block_bytes + off;
+      cudaError_t e = cudaMemcpy2DAsync(dst, p->block_bytes, src, p->block_bytes, width,
+                                        r.second - r.first, cudaMemcpyHostToDevice, p->stream);
+      if (e != cudaSuccess) return set_cuda_error(e, "pool layered memcpy");
+      p->stats[7] += 1;
+    }
+    cudaError_t e = cudaEventRecord(p->ev_layer[g], p->stream);
+    if (e != cudaSuccess) return set_cuda_error(e, "pool layer event record");
+  }
+  p->stats[3] += static_cast<int64_t>(pr.size()) * p->block_bytes;
+  p->pending.clear();
+  p->pend_gpu.clear();
+  p->pend_host.clear();
+  p->pending_dir = 0;
+  p->layered_groups = groups;
+  p->group_layers = lpg;
   return RCB_OK;
 }
 
@@ -314,6 +367,7 @@ int rcb_pool_destroy(rcb_pool* p) {
   if (p->stream) cudaStreamSynchronize(p->stream);
   if (p->ev_done) cudaEventDestroy(p->ev_done);
   if (p->ev_dep) cudaEventDestroy(p->ev_dep);
+  for (cudaEvent_t ev : p->ev_layer) cudaEventDestroy(ev);
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
   if (p->staging) cudaFree(p->staging);
   if (p->host_base) cudaFreeHost(p->host_base);
@@ -567,6 +621,38 @@ int rcb_pool_wait_for(rcb_pool* p, void* stream) {
   cudaError_t e = cudaEventRecord(p->ev_dep, static_cast<cudaStream_t>(stream));
   if (e == cudaSuccess) e = cudaStreamWaitEvent(p->stream, p->ev_dep, 0);
   if (e != cudaSuccess) return set_cuda_error(e, "pool wait_for");
+  return RCB_OK;
+}
+
+int rcb_pool_flush_layered(rcb_pool* p, int32_t layers_per_group) {
+  if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  if (layers_per_group <= 0) return set_error(RCB_ERR_ARG, "layers_per_group must be positive");
+  if (p->swap_mode == RCB_POOL_ACCOUNTING || p->pending_dir != 2 || p->pending.empty())
+    return flush(p);  // nothing to pipeline: a D2H batch (or nothing) issues as usual
+  return flush_layered_h2d(p, std::min(layers_per_group, p->layers));
+}
+
+int rcb_pool_fence_layer(rcb_pool* p, int32_t layer, void* stream) {
+  if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  if (layer < 0 || layer >= p->layers) return set_error(RCB_ERR_ARG, "layer out of range");
+  if (p->swap_mode == RCB_POOL_ACCOUNTING) return RCB_OK;
+  if (!p->pending.empty() || p->layered_groups == 0)
+    return rcb_pool_fence_into(p, stream);  // no layered batch outstanding: full fence
+  const int32_t g = std::min(layer / p->group_layers, p->layered_groups - 1);
+  cudaError_t e = cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), p->ev_layer[g], 0);
+  if (e != cudaSuccess) return set_cuda_error(e, "pool fence_layer");
+  return RCB_OK;
+}
+
+int rcb_pool_drain(rcb_pool* p) {
+  if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  if (p->swap_mode == RCB_POOL_ACCOUNTING) return RCB_OK;
+  if (p->pending_dir == 1) {  // a pending swap-out batch is issued and drained too
+    int rc = flush(p);
+    if (rc != RCB_OK) return rc;
+  }
+  cudaError_t e = cudaStreamSynchronize(p->stream);
+  if (e != cudaSuccess) return set_cuda_error(e, "pool drain");
   return RCB_OK;
 }
 

@@ -88,9 +88,13 @@ class PrefillModel:
                                        device=weights["emb"].device)
 
     def prefill(self, tokens: torch.Tensor, positions: torch.Tensor, slots: torch.Tensor,
-                plan: "kernels.AttnPlan", last_rows: torch.Tensor, stream=None) -> torch.Tensor:
+                plan: "kernels.AttnPlan", last_rows: torch.Tensor, stream=None,
+                layer_fence=None) -> torch.Tensor:
         """tokens/positions/slots: [T] suffix tokens of all requests (packed in plan
-        order); returns fp32 logits [len(last_rows), vocab] of the rows last_rows."""
+        order); returns fp32 logits [len(last_rows), vocab] of the rows last_rows.
+        ``layer_fence(layer)`` (optional) runs before a layer's attention reads the
+        cached pages: the layer-pipelined swap-in waits there for that layer's copies
+        only (BlockPool.fence_layer), the suffix K/V write never touches them."""
         d = self.dims
         s = d.shape
         T = tokens.shape[0]
@@ -107,6 +111,8 @@ class PrefillModel:
                                   slots, self.base, block_tokens=self.bt, n_layers=s.n_layers,
                                   n_kv_heads=s.n_kv_heads, head_dim=s.head_dim, layer=layer,
                                   rope_theta=s.rope_theta, n_q_heads=s.n_q_heads, stream=stream)
+            if layer_fence is not None:
+                layer_fence(layer)
             kernels.prefix_prefill(qkv[:, :qw], attn, plan, self.base, self.nb,
                                    block_tokens=self.bt, n_layers=s.n_layers,
                                    n_kv_heads=s.n_kv_heads, head_dim=s.head_dim, layer=layer,

@@ -201,6 +201,18 @@ class BlockPool:
         self._check(self._lib.rcb_pool_wait_for(self._h, _lib.stream_handle(stream)),
                     "rcb_pool_wait_for")
 
+    def flush_layered(self, layers_per_group: int) -> None:
+        """Issue a pending swap-in batch as per-layer-group DMAs."""
+        self._check(self._lib.rcb_pool_flush_layered(self._h, layers_per_group),
+                    "rcb_pool_flush_layered")
+
+    def fence_layer(self, layer: int, stream) -> None:
+        self._check(self._lib.rcb_pool_fence_layer(self._h, layer, _lib.stream_handle(stream)),
+                    "rcb_pool_fence_layer")
+
+    def drain(self) -> None:
+        self._check(self._lib.rcb_pool_drain(self._h), "rcb_pool_drain")
+
     def sync(self) -> None:
         self._check(self._lib.rcb_pool_sync(self._h), "rcb_pool_sync")
 

@@ -36,6 +36,8 @@ class TimedEngine(TieredEngine):
     def __init__(self, *args, executor, **kwargs) -> None:
         super().__init__(*args, executor=executor, **kwargs)
         self.measured: list[tuple[int, int, int, float, float]] = []  # (req, alpha, beta, profile ms, measured ms)
+        # (req, modeled transfer ms, charged transfer ms, charged prefill ms) per admission
+        self.critical: list[tuple[int, float, float, float]] = []
 
     def _admit(self, gen) -> None:
         held = []
@@ -48,12 +50,18 @@ class TimedEngine(TieredEngine):
             raise RuntimeError(f"_admit scheduled {len(held)} events; the hook expects 1")
         _, kind, rid, payload = held[0]
         modeled = gen.prefill_ms
+        modeled_transfer = gen.transfer_ms
         gen.prefill_ms = float(self.executor.last_ms)
+        if getattr(self.executor, "last_transfer_ms", None) is not None:
+            # the swap-in was executed and is inside the measured time (serial or
+            # layer-pipelined); only its exposed part remains on the critical path
+            gen.transfer_ms = float(self.executor.last_transfer_ms)
         total = gen.transfer_ms + gen.prefill_ms
         chunks = max(1, math.ceil(total / self.config.prefill_chunk_ms)) if total > 0 else 1
         gen.chunk_ms = total / chunks
         gen.chunks_left = chunks
         self.measured.append((gen.request.id, gen.alpha, gen.beta, modeled, gen.prefill_ms))
+        self.critical.append((gen.request.id, modeled_transfer, gen.transfer_ms, gen.prefill_ms))
         self._schedule(self._now + gen.chunk_ms, kind, rid, payload)
 
 
@@ -77,9 +85,28 @@ class ModelExecutor:
     The suffix = the miss documents then the prompt, in the generation's segment order
     (``GenContext``), written into its reserved suffix pages; cached prefix pages (matched
     nodes, swapped in by the pool if they came from the host tier) are read through the
-    block table.  Copies and compute are ordered with the pool's stream fences."""
+    block table.  Copies and compute are ordered with the pool's stream fences.
 
-    def __init__(self, pool, shape: str, *, seed: int = 0, device="cuda") -> None:
+    ``swap_in`` chooses how a generation's host-tier hits (load_to_gpu, tree.py:296-318)
+    reach the prefill:
+      * ``"modeled"``: the pool copies them before the timed region and the reference's
+        ``transfer_time`` (cost_model.py:120-124, measured GB/s) is charged, serially,
+        as ragsim does (simulator.py:505-507);
+      * ``"serial"``: the H2D copies run inside the timed region, then the prefill;
+      * ``"layered"``: the copies are issued per group of ``layers_per_group`` layers and
+        layer l's attention waits only for its group, so the transfer
+        overlaps the earlier layers' compute.
+    In the two measured modes the swap-in time is part of ``last_ms`` and
+    ``last_transfer_ms`` is 0.  Swap-outs issued by the admission are drained before the
+    timed region in every mode (the reference keeps them off the critical path)."""
+
+    def __init__(self, pool, shape: str, *, seed: int = 0, device="cuda", swap_in: str = "modeled",
+                 layers_per_group: int = 4) -> None:
+        if swap_in not in ("modeled", "serial", "layered"):
+            raise ValueError(f"swap_in must be modeled, serial or layered, not {swap_in!r}")
+        self.swap_in = swap_in
+        self.layers_per_group = layers_per_group
+        self.last_transfer_ms = None
         self.dims = DIMS[shape]
         self.pool = pool
         self.w = init_weights(self.dims, seed=seed, device=device)
@@ -108,13 +135,25 @@ class ModelExecutor:
         last = torch.tensor([beta - 1], device=self.device)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        self.pool.fence_into(self.stream)  # swap-ins landed before the prefill reads them
-        e0.record(self.stream)
-        self.model.prefill(tok, idx[:beta], idx[beta:], plan, last)
+        fence = None
+        if self.swap_in == "modeled":
+            self.pool.fence_into(self.stream)  # swap-ins landed before the prefill reads them
+            e0.record(self.stream)
+        else:
+            self.pool.drain()  # this admission's swap-outs: off the critical path
+            e0.record(self.stream)
+            self.pool.wait_for(self.stream)  # copies start inside the timed region
+            if self.swap_in == "layered":
+                self.pool.flush_layered(self.layers_per_group)
+                fence = lambda layer: self.pool.fence_layer(layer, self.stream)  # noqa: E731
+            else:
+                self.pool.fence_into(self.stream)
+        self.model.prefill(tok, idx[:beta], idx[beta:], plan, last, layer_fence=fence)
         e1.record(self.stream)
         self.pool.wait_for(self.stream)  # later swap-outs read the finished pages
         e1.synchronize()
         self.last_ms = e0.elapsed_time(e1)
+        self.last_transfer_ms = None if self.swap_in == "modeled" else 0.0
 
 
 class ProfileExecutor:

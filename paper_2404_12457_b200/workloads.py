@@ -86,6 +86,11 @@ WORKLOADS = {
     # configs[2]: LLaMA2-7B shape, top-5, two-tier cache under memory pressure
     "llama2-7b-top5": Workload("llama2-7b-top5", "llama2-7b", 100_000, 512.0, 0.0, 0.97, 5, 32,
                                40_000, 160_000, 64, batch=12),
+    # configs[2] with repeated questions (query pool, Zipf 1.1 over questions): the
+    # host tier then serves real hits, which the layer-pipelined swap-in targets
+    "llama2-7b-top5-qpool": Workload("llama2-7b-top5-qpool", "llama2-7b", 100_000, 512.0, 0.0,
+                                     0.97, 5, 32, 40_000, 160_000, 64, batch=12,
+                                     query_pool=500, query_zipf_s=1.1),
     # configs[3]: LLaMA2-13B shape, 10M-doc corpus sharded over the GPUs, DSP stages
     # (kvB = 800 KiB/token: a 120K-token tier is 98 GB next to 26 GB of weights)
     "llama2-13b-10m": Workload("llama2-13b-10m", "llama2-13b", 10_000_000, 512.0, 0.0, 0.97, 2,

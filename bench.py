@@ -194,6 +194,32 @@ class Retriever:
         self.launches = 0
         self.bytes_per_scan = corpus_shard.numel() * 2
 
+    def device_ms(self, reps: int = 20) -> float:
+        a, b = self.chunks[0]
+        q = torch.zeros((b - a, self.corpus.shape[1]), dtype=torch.bfloat16, device="cuda")
+        q[:, 0] = 1
+        ids = torch.empty((b - a, self.S, self.k), dtype=torch.int64, device="cuda")
+        sc = torch.empty((b - a, self.S, self.k), dtype=torch.float32, device="cuda")
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            call = lambda: self.kernels.retrieval_topk(  # noqa: E731
+                self.corpus, q, self.k, self.S, self.off, workspace=self.ws[b - a],
+                ids_out=ids, scores_out=sc)
+            call()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                for _ in range(reps):
+                    call()
+        torch.cuda.synchronize()
+        g.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
     def __call__(self, q_local, scan_events=None):
         allq = self.dist.all_gather(q_local).reshape(-1, q_local.shape[1])
         for a, b in self.chunks:
@@ -364,7 +390,10 @@ def run_ours(args, dist: Dist):
         for i in range(K)) / K
     traffic, traffic_src = ncu_traffic("attn_bench")
     scan_ms = [a.elapsed_time(b) for a, b in scan_ev]
-    scan_gbs = retr.bytes_per_scan / (sum(scan_ms) / len(scan_ms) / 1e3) / 1e9 if scan_ms else 0.0
+    # device time per retrieval call (scan + PDL-chained merge) without host launch gaps:
+    # the step's own call replayed back to back from a CUDA graph (corpus >> L2)
+    dev_scan_ms = retr.device_ms()
+    scan_gbs = retr.bytes_per_scan / (dev_scan_ms / 1e3) / 1e9
     d2h = st1["d2h_bytes"] - st0["d2h_bytes"]
     h2d = st1["h2d_bytes"] - st0["h2d_bytes"]
     copy_ms = c0.elapsed_time(c1)
@@ -434,9 +463,13 @@ def run_ours(args, dist: Dist):
                 "flops_per_launch": sum(flops) / len(flops),
                 "share_of_step": round(sum(attn_ms) / elapsed_ms, 4),
             },
-            "retrieval": {"scan_ms_mean": round(sum(scan_ms) / max(1, len(scan_ms)), 4),
+            "retrieval": {"device_ms": round(dev_scan_ms, 4),
                           "achieved_gbs": round(scan_gbs, 1), "peak_gbs": hbm_peak,
-                          "frac": round(scan_gbs / hbm_peak, 4)},
+                          "frac": round(scan_gbs / hbm_peak, 4),
+                          "call_ms_mean": round(sum(scan_ms) / max(1, len(scan_ms)), 4),
+                          "how": "device_ms: 20 calls (scan + merge kernels) replayed from a "
+                                 "CUDA graph, CUDA events; call_ms_mean: in-step event pair "
+                                 "around the host call (includes launch gaps)"},
             "kv_swap": swap,
             "step_swap_bytes": {"d2h": d2h, "h2d": h2d},
             "plan_host_s": round(plan_s, 3),

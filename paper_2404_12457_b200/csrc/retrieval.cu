@@ -8,14 +8,21 @@
 //
 // Corpus GEMM on tcgen05: A = 128 corpus rows x 64-dim atoms (TMA, SW128,
 // 5-stage ring), B = the query batch (<= 64 queries, resident in smem), D in
-// TMEM (double-buffered, 2 x NQ fp32 columns).  Each CTA scans a CONTIGUOUS
-// range of 128-row tiles (so it crosses at most one stage boundary).
+// TMEM (double-buffered, 2 x NQ fp32 columns).
+// Work split: every CTA scans a CONTIGUOUS range of 32-row "quads" (balanced to
+// one quad across the grid: 100K rows over 148 SMs is 21-22 quads per CTA,
+// where whole 128-row tiles would be 5 or 6); a tile is up to 4 quads of one
+// stage segment, loaded as one 128-row TMA box or as 32-row boxes (same SW128
+// smem layout), rows past the tile's end masked in the epilogue.
 // Epilogue (4 warps): TMEM -> registers -> transposed smem tile, then each
 // thread owns one (query, row-part) pair and keeps an exact top-KL list in
-// registers (score desc, id asc; KL = smallest of 2/4/8 >= k).  At a stage
-// boundary the parts of a query are reduced in smem and only k entries per
-// (CTA, query) are written; a merge kernel (one warp per segment,
-// warp-shuffle argmax rounds) produces the per-stage prefix top-k.
+// registers (score desc, id asc; KL = smallest of 2/4/8 >= k).  When a CTA
+// leaves a stage segment its parts are reduced in smem and k entries per
+// query are written to the workspace.  A merge kernel (programmatic dependent
+// launch; one CTA per query, one warp per segment) reads only the CTAs that
+// covered each segment, reduces them with warp-shuffle argmax rounds and emits
+// each stage's prefix top-k.  (A fused last-CTA merge was measured slower: one
+// CTA's dependent L2 round trips over 64 queries cost more than the launch.)
 // Bound: HBM (N * dim * 2 bytes per scan).
 #include <cfloat>
 #include <climits>
@@ -31,11 +38,13 @@ constexpr int kStages = 5;
 constexpr int kKL = 8;  // list length kept per (query, part); k <= kKL
 constexpr int kMaxSeg = 8;
 constexpr int kMaxAtoms = 16;  // dim <= 1024
+constexpr int kQuad = 32;      // rows per quad (CTA range granularity, small TMA box)
 
 struct SegInfo {
   int n_seg;
-  long long bound[kMaxSeg + 1];   // row boundaries
-  int tile_begin[kMaxSeg + 1];    // first global tile of each segment
+  int n_nonempty;
+  long long bound[kMaxSeg + 1];  // row boundaries
+  int quad_begin[kMaxSeg + 1];   // first global quad of each segment
 };
 
 __device__ __forceinline__ bool better(float s1, int i1, float s2, int i2) {
@@ -58,6 +67,32 @@ __device__ __forceinline__ void list_push(float (&ls)[KL], int (&li)[KL], float 
   const bool top = better(sc, id, ls[0], li[0]);
   ls[0] = top ? sc : ls[0];
   li[0] = top ? id : li[0];
+}
+
+// warp-level exact top-k over candidates held as a sorted local list per lane;
+// lane 0 writes entry r to out_s[r] / out_i[r]
+template <int KL>
+__device__ __forceinline__ void warp_topk_emit(float (&ls)[KL], int (&li)[KL], int k,
+                                               float* out_s, int* out_i) {
+  for (int r = 0; r < k; ++r) {
+    const float s = ls[0];
+    const int id = li[0];
+    float bs = s;
+    int bi = id;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float os = __shfl_xor_sync(0xffffffffu, bs, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (better(os, oi, bs, bi)) { bs = os; bi = oi; }
+    }
+    if (lane_id() == 0) { out_s[r] = bs; out_i[r] = bi; }
+    if (bi == id && bs == s && bi != INT_MAX) {  // the winner's lane pops its head
+#pragma unroll
+      for (int i = 0; i < KL - 1; ++i) { ls[i] = ls[i + 1]; li[i] = li[i + 1]; }
+      ls[KL - 1] = -INFINITY;
+      li[KL - 1] = INT_MAX;
+    }
+  }
 }
 
 template <int NQ>
@@ -89,22 +124,45 @@ __device__ __forceinline__ void tmem_ld_row(uint32_t taddr, float (&v)[NQ]) {
   }
 }
 
-// The CTA's contiguous tile range [t_lo, t_hi).
-__device__ __forceinline__ void cta_tiles(int n_tiles, int& t_lo, int& t_hi) {
-  t_lo = (int)(((long long)n_tiles * blockIdx.x) / gridDim.x);
-  t_hi = (int)(((long long)n_tiles * (blockIdx.x + 1)) / gridDim.x);
+// The CTA's contiguous quad range [q_lo, q_hi) and the CTA owning a quad.
+__device__ __forceinline__ void cta_quads(int n_quads, int cta, int& q_lo, int& q_hi) {
+  q_lo = (int)(((long long)n_quads * cta) / gridDim.x);
+  q_hi = (int)(((long long)n_quads * (cta + 1)) / gridDim.x);
 }
+__device__ __forceinline__ int quad_owner(int qd, int n_quads) {
+  return (int)((((long long)qd + 1) * gridDim.x + n_quads - 1) / n_quads) - 1;
+}
+
+// Tile walk over a quad range: a tile is <= 4 quads of one segment.
+struct TileWalk {
+  int q, q_hi, sg;
+  __device__ __forceinline__ bool next(const SegInfo& seg, int& t_sg, long long& r0, long long& r1,
+                                       int& nquads) {
+    if (q >= q_hi) return false;
+    while (sg + 1 < seg.n_seg && q >= seg.quad_begin[sg + 1]) ++sg;
+    int n = q_hi - q;
+    if (n > 4) n = 4;
+    if (n > seg.quad_begin[sg + 1] - q) n = seg.quad_begin[sg + 1] - q;
+    t_sg = sg;
+    r0 = seg.bound[sg] + (long long)(q - seg.quad_begin[sg]) * kQuad;
+    r1 = r0 + (long long)n * kQuad;
+    if (r1 > seg.bound[sg + 1]) r1 = seg.bound[sg + 1];
+    nquads = n;
+    q += n;
+    return true;
+  }
+};
 
 template <int NQ, int KL>
 __global__ void __launch_bounds__(kThreads, 1)
-    topk_scan_kernel(const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_q,
-                     int atoms, int n_tiles, const __grid_constant__ SegInfo seg, int k,
-                     float* __restrict__ part_score, int* __restrict__ part_id,
-                     float* __restrict__ scores_out, int n_queries) {
+    topk_scan_kernel(const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_c32,
+                     const __grid_constant__ CUtensorMap tm_q, int atoms, int n_quads,
+                     const __grid_constant__ SegInfo seg, int k, float* __restrict__ part_score,
+                     int* __restrict__ part_id, float* __restrict__ scores_out, int n_queries) {
   using Lay = Layout<NQ>;
   constexpr int kParts = Lay::kParts;
-  // the merge kernel (launched with programmatic stream serialization) may start launching
-  // now; it waits in griddepcontrol.wait until this grid has completed
+  // the merge kernel (programmatic stream serialization) may launch now; it
+  // waits in griddepcontrol.wait until this grid has completed
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -141,32 +199,33 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  int t_lo, t_hi;
-  cta_tiles(n_tiles, t_lo, t_hi);
-  auto tile_rows = [&](int t, int& sg, long long& r0, long long& r1) {
-    sg = 0;
-    while (sg + 1 < seg.n_seg && t >= seg.tile_begin[sg + 1]) ++sg;
-    r0 = seg.bound[sg] + (long long)(t - seg.tile_begin[sg]) * 128;
-    r1 = r0 + 128;
-    if (r1 > seg.bound[sg + 1]) r1 = seg.bound[sg + 1];
-  };
+  int q_lo, q_hi;
+  cta_quads(n_quads, blockIdx.x, q_lo, q_hi);
 
   if (warp == 4) {
     if (elect_one()) {
       tma_prefetch(&tm_c);
+      tma_prefetch(&tm_c32);
       tma_prefetch(&tm_q);
       mbar_arrive_expect_tx(q_full, atoms * Lay::kAtomQ);
       for (int a = 0; a < atoms; ++a) tma_load_2d(sQ + a * Lay::kAtomQ, &tm_q, q_full, a * 64, 0);
       int it = 0;
-      for (int t = t_lo; t < t_hi; ++t) {
-        int sg;
-        long long r0, r1;
-        tile_rows(t, sg, r0, r1);
+      TileWalk tw{q_lo, q_hi, 0};
+      int sg, nq4;
+      long long r0, r1;
+      while (tw.next(seg, sg, r0, r1, nq4)) {
         for (int a = 0; a < atoms; ++a, ++it) {
           const int st = it % kStages;
           mbar_wait(&empty[st], ((it / kStages) & 1) ^ 1);
-          mbar_arrive_expect_tx(&full[st], Lay::kA);
-          tma_load_2d(sA + st * Lay::kA, &tm_c, &full[st], a * 64, (int)r0);
+          uint8_t* dst = sA + st * Lay::kA;
+          if (nq4 == 4) {
+            mbar_arrive_expect_tx(&full[st], Lay::kA);
+            tma_load_2d(dst, &tm_c, &full[st], a * 64, (int)r0);
+          } else {
+            mbar_arrive_expect_tx(&full[st], nq4 * kQuad * 128);
+            for (int j = 0; j < nq4; ++j)
+              tma_load_2d(dst + j * kQuad * 128, &tm_c32, &full[st], a * 64, (int)r0 + j * kQuad);
+          }
         }
       }
     }
@@ -178,7 +237,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(q_full, 0);
       tc_fence_after();
       int it = 0, li = 0;
-      for (int t = t_lo; t < t_hi; ++t, ++li) {
+      TileWalk tw{q_lo, q_hi, 0};
+      int sg, nq4;
+      long long r0, r1;
+      for (; tw.next(seg, sg, r0, r1, nq4); ++li) {
         const int buf = li & 1;
         mbar_wait(&acc_empty[buf], ((li >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -208,7 +270,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int i = 0; i < KL; ++i) { ls[i] = -INFINITY; li_[i] = INT_MAX; }
     int cur_seg = -1;
-    unsigned flushed = 0;
     // reduce the kParts lists of each query in smem, write k entries for this CTA
     auto flush = [&](int sg) {
       named_bar_sync(1, 128);  // sT free
@@ -224,8 +285,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int p = 1; p < kParts; ++p)
 #pragma unroll
           for (int i = 0; i < KL; ++i) list_push<KL>(ls, li_, ms[(p * NQ + q) * KL + i], mi[(p * NQ + q) * KL + i]);
-        // workspace [segment][query][CTA][k]: the merge warp of (segment, query) reads its
-        // grid x k candidates contiguously
+        // workspace [segment][query][CTA][k]: the merging warp of (segment, query)
+        // reads the covering CTAs' candidates contiguously
         const long long base = (((long long)sg * NQ + q) * gridDim.x + blockIdx.x) * k;
 #pragma unroll
         for (int i = 0; i < KL; ++i)
@@ -236,13 +297,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
 #pragma unroll
       for (int i = 0; i < KL; ++i) { ls[i] = -INFINITY; li_[i] = INT_MAX; }
-      flushed |= 1u << sg;
     };
     int li = 0;
-    for (int t = t_lo; t < t_hi; ++t, ++li) {
-      int sg;
-      long long r0, r1;
-      tile_rows(t, sg, r0, r1);
+    TileWalk tw{q_lo, q_hi, 0};
+    int sg, nq4;
+    long long r0, r1;
+    for (; tw.next(seg, sg, r0, r1, nq4); ++li) {
       if (sg != cur_seg) {
         if (cur_seg >= 0) flush(cur_seg);
         cur_seg = sg;
@@ -275,8 +335,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (cur_seg >= 0) flush(cur_seg);
-    for (int sg = 0; sg < seg.n_seg; ++sg)
-      if (!(flushed & (1u << sg))) flush(sg);
     tc_fence_before();
   }
   __syncthreads();
@@ -286,51 +344,34 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// warp-level exact top-k over candidates held as a sorted local list per lane
-template <int KL>
-__device__ __forceinline__ void warp_topk_emit(float (&ls)[KL], int (&li)[KL], int k,
-                                               float* out_s, int* out_i) {
-  for (int r = 0; r < k; ++r) {
-    const float s = ls[0];
-    const int id = li[0];
-    float bs = s;
-    int bi = id;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float os = __shfl_xor_sync(0xffffffffu, bs, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (better(os, oi, bs, bi)) { bs = os; bi = oi; }
-    }
-    if (lane_id() == 0) { out_s[r] = bs; out_i[r] = bi; }
-    if (bi == id && bs == s && bi != INT_MAX) {  // the winner's lane pops its head
-#pragma unroll
-      for (int i = 0; i < KL - 1; ++i) { ls[i] = ls[i + 1]; li[i] = li[i + 1]; }
-      ls[KL - 1] = -INFINITY;
-      li[KL - 1] = INT_MAX;
-    }
-  }
-}
-
-// grid = n_queries, block = 32 * n_seg; warp s reduces segment s (grid_scan x k
-// candidates), then emits stage s = prefix merge of segments 0..s
+// grid = n_queries, block = 32 * n_seg; warp s reduces the candidates of the
+// scan CTAs that covered segment s, then emits stage s = prefix merge of 0..s
 __global__ void topk_merge_kernel(const float* __restrict__ part_score,
-                                  const int* __restrict__ part_id, int n_parts, int NQ, int n_seg,
-                                  int k, long long id_offset, long long* __restrict__ ids_out,
+                                  const int* __restrict__ part_id, int scan_grid, int n_quads,
+                                  int NQ, const __grid_constant__ SegInfo seg, int k,
+                                  long long id_offset, long long* __restrict__ ids_out,
                                   float* __restrict__ scores_out) {
   __shared__ float seg_s[kMaxSeg][kKL];
   __shared__ int seg_i[kMaxSeg][kKL];
   __shared__ float out_s[kMaxSeg][kKL];
   __shared__ int out_i[kMaxSeg][kKL];
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // the scan grid completed
   const int q = blockIdx.x;
   const int s = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int n_seg = seg.n_seg;
+  // covering CTAs of segment s (the scan's quad_owner with the scan's grid)
+  auto owner = [&](int qd) {
+    return (int)((((long long)qd + 1) * scan_grid + n_quads - 1) / n_quads) - 1;
+  };
+  const bool empty = seg.quad_begin[s + 1] == seg.quad_begin[s];
+  const int c_lo = empty ? 0 : owner(seg.quad_begin[s]);
+  const int n_cand = empty ? 0 : (owner(seg.quad_begin[s + 1] - 1) - c_lo + 1) * k;
+  const long long base = (((long long)s * NQ + q) * scan_grid + c_lo) * k;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the scan grid completed
   float ls[kKL];
   int li[kKL];
 #pragma unroll
   for (int i = 0; i < kKL; ++i) { ls[i] = -INFINITY; li[i] = INT_MAX; }
-  const int n_cand = n_parts * k;
-  const long long base = ((long long)s * NQ + q) * n_cand;  // [segment][query][CTA][k]
   // coalesced, 8 loads in flight per lane before the list updates
   for (int c0 = 0; c0 < n_cand; c0 += 32 * 8) {
     float cs[8];
@@ -427,53 +468,71 @@ int num_sms() {
 
 int nq_pad(int n) { return n <= 16 ? 16 : (n <= 32 ? 32 : 64); }
 
-void make_segments(int64_t n_rows, int n_stages, SegInfo& seg, int& n_tiles) {
+void make_segments(int64_t n_rows, int n_stages, SegInfo& seg, int& n_quads) {
   seg.n_seg = n_stages;
-  int t = 0;
+  seg.n_nonempty = 0;
+  int q = 0;
   for (int s = 0; s <= n_stages; ++s) seg.bound[s] = (long long)((n_rows * s) / n_stages);
   for (int s = 0; s < n_stages; ++s) {
-    seg.tile_begin[s] = t;
+    seg.quad_begin[s] = q;
     const long long len = seg.bound[s + 1] - seg.bound[s];
-    t += (int)((len + 127) / 128);
+    q += (int)((len + kQuad - 1) / kQuad);
+    seg.n_nonempty += len > 0;
   }
-  seg.tile_begin[n_stages] = t;
-  for (int s = n_stages + 1; s <= kMaxSeg; ++s) { seg.bound[s] = n_rows; seg.tile_begin[s] = t; }
-  n_tiles = t;
+  seg.quad_begin[n_stages] = q;
+  for (int s = n_stages + 1; s <= kMaxSeg; ++s) { seg.bound[s] = n_rows; seg.quad_begin[s] = q; }
+  n_quads = q;
 }
 
-int grid_for(int n_tiles) {
+int grid_for(int n_quads) {
   const int g = num_sms();
-  return n_tiles < g ? (n_tiles > 0 ? n_tiles : 1) : g;
+  return n_quads < g ? (n_quads > 0 ? n_quads : 1) : g;
+}
+
+// workspace: partial lists [n_seg][NQ][grid][k] (score f32, then id i32)
+int64_t part_entries(int64_t n_rows, int n_queries, int k, int n_stages) {
+  SegInfo seg;
+  int n_quads;
+  make_segments(n_rows, n_stages, seg, n_quads);
+  return int64_t(n_stages) * nq_pad(n_queries) * grid_for(n_quads) * (k < 1 ? 1 : k);
 }
 
 template <int NQ, int KL>
-int run_scan_kl(const CUtensorMap& tc, const CUtensorMap& tq, int atoms, int n_tiles,
-                const SegInfo& seg, int k, float* part_score, int* part_id, float* scores_out,
-                int n_queries, int grid, cudaStream_t stream) {
+int run_scan_kl(const CUtensorMap& tc, const CUtensorMap& tc32, const CUtensorMap& tq, int atoms,
+                int n_quads, const SegInfo& seg, int k, float* part_score, int* part_id,
+                float* scores_out, int n_queries, int grid,
+                cudaStream_t stream) {
   const uint32_t smem = Layout<NQ>::total(atoms);
   auto kern = topk_scan_kernel<NQ, KL>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return set_cuda_error(e, "retrieval smem attr");
-  kern<<<grid, kThreads, smem, stream>>>(tc, tq, atoms, n_tiles, seg, k, part_score, part_id,
+  static uint32_t smem_set = 0;  // per instantiation: set the attribute once per size
+  if (smem > smem_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return set_cuda_error(e, "retrieval smem attr");
+    smem_set = smem;
+  }
+  kern<<<grid, kThreads, smem, stream>>>(tc, tc32, tq, atoms, n_quads, seg, k, part_score, part_id,
                                          scores_out, n_queries);
-  e = cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "retrieval scan launch");
   return RCB_OK;
 }
 
 template <int NQ>
 int run_scan(const void* corpus, int64_t n_rows, int dim, const void* queries, int n_queries,
-             int n_stages, int k, float* part_score, int* part_id, float* scores_out, int grid,
-             cudaStream_t stream) {
+             int n_stages, int k, float* part_score, int* part_id, float* scores_out,
+             int grid, cudaStream_t stream) {
   SegInfo seg;
-  int n_tiles;
-  make_segments(n_rows, n_stages, seg, n_tiles);
-  CUtensorMap tc, tq;
+  int n_quads;
+  make_segments(n_rows, n_stages, seg, n_quads);
+  CUtensorMap tc, tc32, tq;
   {
     const uint64_t dims[2] = {(uint64_t)dim, (uint64_t)n_rows};
     const uint64_t strides[1] = {(uint64_t)dim * 2};
     const uint32_t box[2] = {64, 128};
     int rc = encode_tma_bf16(&tc, corpus, 2, dims, strides, box);
+    if (rc != RCB_OK) return rc;
+    const uint32_t box32[2] = {64, (uint32_t)kQuad};
+    rc = encode_tma_bf16(&tc32, corpus, 2, dims, strides, box32);
     if (rc != RCB_OK) return rc;
   }
   {
@@ -485,15 +544,15 @@ int run_scan(const void* corpus, int64_t n_rows, int dim, const void* queries, i
   }
   const int atoms = dim / 64;
   if (k <= 2)
-    return run_scan_kl<NQ, 2>(tc, tq, atoms, n_tiles, seg, k, part_score, part_id, scores_out, n_queries, grid, stream);
+    return run_scan_kl<NQ, 2>(tc, tc32, tq, atoms, n_quads, seg, k, part_score, part_id, scores_out, n_queries, grid, stream);
   if (k <= 4)
-    return run_scan_kl<NQ, 4>(tc, tq, atoms, n_tiles, seg, k, part_score, part_id, scores_out, n_queries, grid, stream);
-  return run_scan_kl<NQ, 8>(tc, tq, atoms, n_tiles, seg, k, part_score, part_id, scores_out, n_queries, grid, stream);
+    return run_scan_kl<NQ, 4>(tc, tc32, tq, atoms, n_quads, seg, k, part_score, part_id, scores_out, n_queries, grid, stream);
+  return run_scan_kl<NQ, 8>(tc, tc32, tq, atoms, n_quads, seg, k, part_score, part_id, scores_out, n_queries, grid, stream);
 }
 
 int scan(const void* corpus, int64_t n_rows, int dim, const void* queries, int n_queries,
-         int n_stages, int k, float* part_score, int* part_id, float* scores_out, int grid,
-         cudaStream_t stream) {
+         int n_stages, int k, float* part_score, int* part_id, float* scores_out,
+         int grid, cudaStream_t stream) {
   switch (nq_pad(n_queries)) {
     case 16: return run_scan<16>(corpus, n_rows, dim, queries, n_queries, n_stages, k, part_score, part_id, scores_out, grid, stream);
     case 32: return run_scan<32>(corpus, n_rows, dim, queries, n_queries, n_stages, k, part_score, part_id, scores_out, grid, stream);
@@ -514,15 +573,10 @@ int check_args(int64_t n_rows, int dim, int n_queries, int n_stages) {
 
 using namespace rcb;
 
-// workspace: per (stage segment, scan CTA, padded query) k entries of (score, id)
 extern "C" int64_t rcb_retrieval_workspace_bytes(int64_t n_rows, int32_t n_queries, int32_t k,
                                                  int32_t n_stages) {
-  ret::SegInfo seg;
-  int n_tiles;
-  ret::make_segments(n_rows, n_stages, seg, n_tiles);
-  const int grid = ret::grid_for(n_tiles);
-  const int nq = ret::nq_pad(n_queries);
-  return int64_t(n_stages) * grid * nq * (k < 1 ? 1 : k) * 8;
+  if (n_rows <= 0 || n_stages <= 0 || n_stages > ret::kMaxSeg) return 16;
+  return ret::part_entries(n_rows, n_queries, k, n_stages) * 8;
 }
 
 extern "C" int rcb_retrieval_topk(const void* corpus_dev, int64_t n_rows, int32_t dim,
@@ -533,15 +587,14 @@ extern "C" int rcb_retrieval_topk(const void* corpus_dev, int64_t n_rows, int32_
   int rc = ret::check_args(n_rows, dim, n_queries, n_stages);
   if (rc != RCB_OK) return rc;
   if (k < 1 || k > ret::kKL) return set_error(RCB_ERR_ARG, "1 <= k <= 8");
-  const int64_t need = rcb_retrieval_workspace_bytes(n_rows, n_queries, k, n_stages);
-  if (workspace_bytes < need) return set_error(RCB_ERR_ARG, "retrieval workspace too small");
+  const int64_t entries = ret::part_entries(n_rows, n_queries, k, n_stages);
+  if (workspace_bytes < entries * 8) return set_error(RCB_ERR_ARG, "retrieval workspace too small");
   ret::SegInfo seg;
-  int n_tiles;
-  ret::make_segments(n_rows, n_stages, seg, n_tiles);
-  const int grid = ret::grid_for(n_tiles);
-  const int nq = ret::nq_pad(n_queries);
+  int n_quads;
+  ret::make_segments(n_rows, n_stages, seg, n_quads);
+  const int grid = ret::grid_for(n_quads);
   float* ps = static_cast<float*>(workspace_dev);
-  int* pi = reinterpret_cast<int*>(ps + int64_t(n_stages) * grid * nq * k);
+  int* pi = reinterpret_cast<int*>(ps + entries);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   rc = ret::scan(corpus_dev, n_rows, dim, queries_dev, n_queries, n_stages, k, ps, pi, nullptr,
                  grid, st);
@@ -557,7 +610,8 @@ extern "C" int rcb_retrieval_topk(const void* corpus_dev, int64_t n_rows, int32_
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, ret::topk_merge_kernel, static_cast<const float*>(ps),
-                                     static_cast<const int*>(pi), grid, nq, n_stages, k,
+                                     static_cast<const int*>(pi), grid, n_quads,
+                                     ret::nq_pad(n_queries), seg, k,
                                      static_cast<long long>(id_offset),
                                      reinterpret_cast<long long*>(ids_out_dev), scores_out_dev);
   if (e == cudaSuccess) e = cudaGetLastError();
@@ -570,18 +624,17 @@ extern "C" int rcb_retrieval_scores(const void* corpus_dev, int64_t n_rows, int3
                                     float* scores_out_dev, void* stream) {
   int rc = ret::check_args(n_rows, dim, n_queries, 1);
   if (rc != RCB_OK) return rc;
-  const int64_t ws = rcb_retrieval_workspace_bytes(n_rows, n_queries, 1, 1);
+  const int64_t entries = ret::part_entries(n_rows, n_queries, 1, 1);
   ret::SegInfo seg;
-  int n_tiles;
-  ret::make_segments(n_rows, 1, seg, n_tiles);
-  const int grid = ret::grid_for(n_tiles);
-  const int nq = ret::nq_pad(n_queries);
+  int n_quads;
+  ret::make_segments(n_rows, 1, seg, n_quads);
+  const int grid = ret::grid_for(n_quads);
   void* buf = nullptr;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = cudaMallocAsync(&buf, ws, st);
+  cudaError_t e = cudaMallocAsync(&buf, entries * 8, st);
   if (e != cudaSuccess) return set_cuda_error(e, "retrieval scores workspace");
   float* ps = static_cast<float*>(buf);
-  int* pi = reinterpret_cast<int*>(ps + int64_t(grid) * nq);
+  int* pi = reinterpret_cast<int*>(ps + entries);
   rc = ret::scan(corpus_dev, n_rows, dim, queries_dev, n_queries, 1, 1, ps, pi, scores_out_dev,
                  grid, st);
   cudaFreeAsync(buf, st);

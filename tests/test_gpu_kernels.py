@@ -69,6 +69,9 @@ def test_block_copy_pinned_host_roundtrip():
 # ---------------------------------------------------------------- retrieval
 @pytest.mark.parametrize("n_rows,b,k,stages", [
     (10000, 5, 2, 4), (10007, 16, 5, 4), (3000, 40, 8, 1), (20011, 64, 5, 4), (700, 64, 2, 8),
+    # quad-balanced ranges / merge edge cases: empty stage segments (rows < stages), fewer rows than k,
+    # ~one 32-row quad per CTA, many tiles per CTA with ragged quads
+    (5, 3, 2, 8), (33, 3, 4, 8), (4741, 7, 3, 3), (150001, 64, 2, 4), (262144, 33, 1, 5),
 ])
 def test_retrieval_scores_and_topk_exact(n_rows, b, k, stages):
     corpus = synth.corpus_int(n_rows, seed=n_rows)
@@ -83,6 +86,25 @@ def test_retrieval_scores_and_topk_exact(n_rows, b, k, stages):
     o_ids, o_sc = topk_oracle.staged_topk(corpus, q, k, stages, id_offset=1000)
     assert np.array_equal(ids.cpu().numpy(), o_ids)
     assert np.array_equal(sc.cpu().numpy().astype(np.float64), o_sc)
+
+
+def test_retrieval_workspace_reuse():
+    """Back-to-back calls on one workspace (different queries, scan and merge kernels
+    chained by programmatic dependent launch) stay exact."""
+    corpus = synth.corpus_int(30011, seed=4)
+    c_dev = torch.from_numpy(corpus.astype(np.float32)).to("cuda", torch.bfloat16)
+    ws = kernels.RetrievalWorkspace(corpus.shape[0], 24, 4, 4)
+    outs = []
+    for rep in range(5):
+        q = np.random.default_rng(100 + rep).integers(-200, 201, size=(24, synth.EMB_DIM))
+        q = q.astype(np.float64)
+        q_dev = torch.from_numpy(q.astype(np.float32)).to("cuda", torch.bfloat16)
+        outs.append((q, kernels.retrieval_topk(c_dev, q_dev, 4, 4, workspace=ws)))
+    torch.cuda.synchronize()
+    for q, (ids, sc) in outs:
+        o_ids, o_sc = topk_oracle.staged_topk(corpus, q, 4, 4)
+        assert np.array_equal(ids.cpu().numpy(), o_ids)
+        assert np.array_equal(sc.cpu().numpy().astype(np.float64), o_sc)
 
 
 def test_retrieval_ties_break_by_id():

@@ -148,6 +148,37 @@ def bench_retrieval():
                                                          scores_out=sc))
         emit(kind="retrieval_topk", rows=n, dim=synth.EMB_DIM, queries=b, ms=med,
              gbs=n * synth.EMB_DIM * 2 / med / 1e6, frac_hbm=n * synth.EMB_DIM * 2 / med / 1e6 / hbm)
+        if NCU:
+            continue
+        # device-side time without host launch gaps: 20 calls captured in a CUDA graph
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            kernels.retrieval_topk(corpus, q, 2, 4, workspace=ws, ids_out=ids, scores_out=sc)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(20):
+                    kernels.retrieval_topk(corpus, q, 2, 4, workspace=ws, ids_out=ids,
+                                           scores_out=sc)
+        torch.cuda.synchronize()
+        g.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        gms = e0.elapsed_time(e1) / 20
+        # host cost of one call (no sync): wall time of 200 back-to-back calls
+        import time as _t
+        torch.cuda.synchronize()
+        t0 = _t.perf_counter()
+        for _ in range(200):
+            kernels.retrieval_topk(corpus, q, 2, 4, workspace=ws, ids_out=ids, scores_out=sc)
+        host_us = (_t.perf_counter() - t0) / 200 * 1e6
+        torch.cuda.synchronize()
+        emit(kind="retrieval_topk_graph", rows=n, queries=b, ms=gms,
+             gbs=n * synth.EMB_DIM * 2 / gms / 1e6, frac_hbm=n * synth.EMB_DIM * 2 / gms / 1e6 / hbm,
+             host_us_per_call=round(host_us, 1))
 
 
 def bench_attn():

@@ -167,14 +167,19 @@ int rcb_rope_table(void* table_dev, int32_t max_pos, int32_t head_dim, float rop
  *   work_dev    : int32 [n_work][8] = {q_start, q_len, q_pos0, blk_begin, blk_count,
  *                 q_pair, kv_head, n0 | half0 << 15 | n1 << 16 | half1 << 31}: two adjacent
  *                 128-row query tiles per item and the KV tiles each needs (built by
- *                 rcb_attn_plan, heaviest first) */
+ *                 rcb_attn_plan, heaviest first)
+ *   work_flags  : RCB_WORK_SPLIT_ONLY if every item has n1 == 0 (one query tile: decode
+ *                 steps, short prompts over cached documents); the kernel then keeps one
+ *                 Q tile per item buffer and runs a deeper K/V ring (HBM-bound launches) */
+#define RCB_WORK_SPLIT_ONLY 1
 int rcb_prefix_prefill(const void* q, int64_t q_row_stride, void* o, int32_t total_q_tokens,
                        int32_t n_q_heads, const void* kv_pool, int64_t num_pool_blocks,
                        int32_t block_tokens, int32_t n_layers, int32_t n_kv_heads,
                        int32_t head_dim, int32_t layer, const int32_t* req_meta_dev,
                        const int32_t* blk_ids_dev, const int32_t* blk_valid_dev,
                        const int32_t* blk_pos_dev, const int32_t* work_dev, int32_t n_work,
-                       float softmax_scale, const void* rope_table_dev, void* stream);
+                       float softmax_scale, const void* rope_table_dev, int32_t work_flags,
+                       void* stream);
 /* host-side work planner for rcb_prefix_prefill: writes up to cap items (8 int32 each) into
  * work_out (heaviest first) and returns the count in n_work_out.  Inputs are the
  * host copies of req_meta / blk_valid / blk_pos. */

@@ -32,6 +32,8 @@ RCB_SWAP_ZEROCOPY = 1
 RCB_SWAP_DMA = 2
 RCB_POOL_ACCOUNTING = 3
 
+RCB_WORK_SPLIT_ONLY = 1
+
 
 class RcbUnavailable(RuntimeError):
     """The native library is not built / cannot be loaded (no CPU fallback exists)."""
@@ -87,7 +89,7 @@ SIGNATURES = [
     ("rcb_prefix_prefill", c_int, [c_void_p, c_int64, c_void_p, c_int32, c_int32, c_void_p,
                                    c_int64, c_int32, c_int32, c_int32, c_int32, c_int32,
                                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32,
-                                   c_float, c_void_p, c_void_p]),
+                                   c_float, c_void_p, c_int32, c_void_p]),
     ("rcb_attn_plan", c_int, [_p32, c_int32, _p32, _p32, c_int32, c_int32, c_int32, _p32,
                               c_int32, _p32]),
     ("rcb_retrieval_workspace_bytes", c_int64, [c_int64, c_int32, c_int32, c_int32]),

@@ -75,16 +75,22 @@ enum Bar {
   kKVFull0 = 30  // [kStages] full, then [kStages] empty
 };
 
-template <int HD, int BT>
+// SPLIT: every item of the launch is a split item (one query tile: decode steps and
+// short prompts over cached documents, HBM-bound).  Q then needs one tile per item
+// buffer, and the freed 64 KB (HD = 128) deepens the K/V ring from 3 to 5 stages:
+// a V stage stays held from its load until the PV after its tile's softmax, so the
+// ring depth is what bounds the bytes in flight per SM on these launches.
+template <int HD, int BT, bool SPLIT>
 struct Smem {
   static constexpr uint32_t kHalves = HD / 64;
   static constexpr uint32_t kQ = kHalves * 16384;   // one query tile
   static constexpr uint32_t kKV = kHalves * 16384;  // one K or V tile
-  static constexpr int kStages = HD == 128 ? 3 : 6;  // K/V ring depth
+  static constexpr uint32_t kQT = SPLIT ? 1 : 2;    // query tiles per item buffer
+  static constexpr int kStages = HD == 128 ? (SPLIT ? 5 : 3) : (SPLIT ? 8 : 6);  // K/V ring
   static constexpr int kBPT = kKeys / BT;
   static constexpr int kMetaSlots = 4;
-  static constexpr uint32_t offQ = 0;                       // [2 items][2 tiles]
-  static constexpr uint32_t offKV = offQ + 4 * kQ;          // [kStages]
+  static constexpr uint32_t offQ = 0;                       // [2 items][kQT tiles]
+  static constexpr uint32_t offKV = offQ + 2 * kQT * kQ;    // [kStages]
   static constexpr uint32_t offMeta = offKV + kStages * kKV;  // int [kMetaSlots][2][kBPT]
   static constexpr uint32_t offL = offMeta + kMetaSlots * 2 * kBPT * 4;  // float2 [2][128]
   static constexpr uint32_t offBar = offL + 2 * 128 * 8;
@@ -141,7 +147,7 @@ __device__ __forceinline__ Item load_item(const int* __restrict__ work, int idx)
 // counter s runs across items, so the K/V ring, mask-metadata ring and S/P handshakes
 // keep their phase; Q (smem) is double buffered per item, O_w single buffered (the
 // epilogue frees O_w before the next item's first PV into it).
-template <int HD, int G, int BT>
+template <int HD, int G, int BT, bool SPLIT>
 __global__ void __launch_bounds__(kThreads, 1)
     prefix_prefill_kernel(const __grid_constant__ CUtensorMap tm_q,
                           const __grid_constant__ CUtensorMap tm_kv,
@@ -149,7 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                           const int* __restrict__ blk_ids, const int* __restrict__ blk_valid,
                           const int* __restrict__ blk_pos, const int* __restrict__ work,
                           int n_work, float scale_log2, const float2* __restrict__ rope) {
-  using S = Smem<HD, BT>;
+  using S = Smem<HD, BT, SPLIT>;
   constexpr int TQ = kRows / G;  // tokens per query tile
   constexpr int BPT = S::kBPT;
   constexpr int NS = S::kStages;
@@ -216,11 +222,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue_q = [&](int idx, int ii) {
         const Item it = load_item(work, idx);
         const int qb = ii & 1;
-        mbar_arrive_expect_tx(&bar[kQFull0 + qb], 2 * S::kQ);
-        for (int w = 0; w < 2; ++w)
+        if (SPLIT && !it.split()) __trap();  // the host promised split items only
+        mbar_arrive_expect_tx(&bar[kQFull0 + qb], S::kQT * S::kQ);
+        for (int w = 0; w < (int)S::kQT; ++w)
           for (int h = 0; h < (int)S::kHalves; ++h)
             // an empty Q1 (never read) reloads Q0's rows: no box lies wholly out of bounds
-            tma_load_3d(sQ + (qb * 2 + w) * S::kQ + h * 16384, &tm_q, &bar[kQFull0 + qb],
+            tma_load_3d(sQ + (qb * S::kQT + w) * S::kQ + h * 16384, &tm_q, &bar[kQFull0 + qb],
                         h * 64, it.kvh * G, it.q_start + (2 * it.qp + (it.n1 > 0 ? w : 0)) * TQ);
       };
       auto load_kv = [&](int u, int kv, const int (&ids)[BPT], int kvh) {
@@ -357,21 +364,40 @@ __global__ void __launch_bounds__(kThreads, 1)
             k_ready = true;
           };
           // S_w is overwritten by QK_w(s) only after PV_w(s-1) (its P reader) was issued;
-          // tcgen05.mma executes in issue order
-          if (p_has[0]) issue_pv(0);
-          const int pc0 = c[0];
-          if (h0) {
-            need_k();
-            issue_qk(0, qb * 2, ku, it.half(0, j));
-            TRACE(s, 9);
-          }
-          if (p_has[1]) issue_pv(1);
-          if (p_any) umma_commit(&kv_empty[p_vu % NS]);  // V(s-1) no longer read
-          const int pc1 = c[1];
-          if (h1) {
-            need_k();
-            issue_qk(1, qb * 2 + it.qtile(1), ku, it.half(1, j));
-            TRACE(s, 11);
+          // tcgen05.mma executes in issue order.  Pair items: PV0 QK0 PV1 QK1 (each
+          // softmax overlaps the other tile's MMAs).  Split items alternate WGs over the
+          // steps, so on a WG1 step QK1 goes FIRST and the pending PV0 (which waits for
+          // WG0's softmax) after it: the two WGs' softmaxes then overlap instead of
+          // forming one chain through the MMA warp.
+          int pc0 = c[0], pc1 = c[1];
+          auto qk0 = [&]() {
+            pc0 = c[0];
+            if (h0) {
+              need_k();
+              issue_qk(0, qb * S::kQT, ku, it.half(0, j));
+              TRACE(s, 9);
+            }
+          };
+          auto qk1 = [&]() {
+            pc1 = c[1];
+            if (h1) {
+              need_k();
+              issue_qk(1, qb * S::kQT + (SPLIT ? 0 : it.qtile(1)), ku, it.half(1, j));
+              TRACE(s, 11);
+            }
+          };
+          if (SPLIT && (j & 1)) {  // WG1 step (split-only launch; mixed launches keep one order)
+            if (p_has[1]) issue_pv(1);
+            qk1();
+            if (p_has[0]) issue_pv(0);
+            if (p_any) umma_commit(&kv_empty[p_vu % NS]);  // V(s-1) no longer read
+            qk0();
+          } else {
+            if (p_has[0]) issue_pv(0);
+            qk0();
+            if (p_has[1]) issue_pv(1);
+            if (p_any) umma_commit(&kv_empty[p_vu % NS]);  // V(s-1) no longer read
+            qk1();
           }
           umma_commit(&kv_empty[ku % NS]);  // K(s) no longer read
           if (j == n - 1) umma_commit(&bar[kQEmpty0 + qb]);  // Q tiles no longer read
@@ -596,7 +622,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int e = 0; e < 4; ++e) nxt[e] = __ldg(t + e);
         }
         const int w = u / U, tt = (u % U) / CP, cp = u % CP;
-        const uint32_t qbase = smem_u32(sQ) + (qb * 2 + w) * S::kQ;
+        const uint32_t qbase = smem_u32(sQ) + (qb * S::kQT + w) * S::kQ;
         const int i0 = cp * 8, j0 = i0 + HD / 2;
         // (cos, sin) of elements (2e, 2e+1) as f32x2 pairs, shared by the G rows
         uint64_t c2[4], s2[4], ns2[4];
@@ -723,15 +749,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int HD, int G, int BT>
-cudaError_t launch_t(const CUtensorMap& tq, const CUtensorMap& tkv, void* out, int n_q_heads,
+template <int HD, int G, int BT, bool SPLIT>
+cudaError_t launch_s(const CUtensorMap& tq, const CUtensorMap& tkv, void* out, int n_q_heads,
                      int layer, const int* blk_ids, const int* blk_valid,
                      const int* blk_pos, const int* work, int n_work, float scale_log2,
                      const float2* rope, cudaStream_t stream) {
-  auto kern = prefix_prefill_kernel<HD, G, BT>;
-  const uint32_t smem = Smem<HD, BT>::kTotal;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
+  auto kern = prefix_prefill_kernel<HD, G, BT, SPLIT>;
+  const uint32_t smem = Smem<HD, BT, SPLIT>::kTotal;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
   static int sms = 0;
   if (sms == 0) {
     int dev = 0;
@@ -746,30 +776,39 @@ cudaError_t launch_t(const CUtensorMap& tq, const CUtensorMap& tkv, void* out, i
   return cudaGetLastError();
 }
 
+template <int HD, int G, int BT>
+cudaError_t launch_t(bool split, const CUtensorMap& tq, const CUtensorMap& tkv, void* out,
+                     int n_q_heads, int layer, const int* bi, const int* bv, const int* bp,
+                     const int* work, int n_work, float sl2, const float2* rope,
+                     cudaStream_t st) {
+  return split ? launch_s<HD, G, BT, true>(tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st)
+               : launch_s<HD, G, BT, false>(tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
+}
+
 template <int HD, int G>
-cudaError_t launch_bt(int bt, const CUtensorMap& tq, const CUtensorMap& tkv, void* out,
+cudaError_t launch_bt(bool split, int bt, const CUtensorMap& tq, const CUtensorMap& tkv, void* out,
                       int n_q_heads, int layer, const int* bi, const int* bv,
                       const int* bp, const int* work, int n_work, float sl2, const float2* rope,
                       cudaStream_t st) {
   switch (bt) {
-    case 16: return launch_t<HD, G, 16>(tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
-    case 32: return launch_t<HD, G, 32>(tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
-    case 64: return launch_t<HD, G, 64>(tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
-    case 128: return launch_t<HD, G, 128>(tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
+    case 16: return launch_t<HD, G, 16>(split, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
+    case 32: return launch_t<HD, G, 32>(split, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
+    case 64: return launch_t<HD, G, 64>(split, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
+    case 128: return launch_t<HD, G, 128>(split, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
 template <int HD>
-cudaError_t launch_g(int g, int bt, const CUtensorMap& tq, const CUtensorMap& tkv, void* out,
+cudaError_t launch_g(bool split, int g, int bt, const CUtensorMap& tq, const CUtensorMap& tkv, void* out,
                      int n_q_heads, int layer, const int* bi, const int* bv,
                      const int* bp, const int* work, int n_work, float sl2, const float2* rope,
                      cudaStream_t st) {
   switch (g) {
-    case 1: return launch_bt<HD, 1>(bt, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
-    case 2: return launch_bt<HD, 2>(bt, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
-    case 4: return launch_bt<HD, 4>(bt, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
-    case 8: return launch_bt<HD, 8>(bt, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
+    case 1: return launch_bt<HD, 1>(split, bt, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
+    case 2: return launch_bt<HD, 2>(split, bt, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
+    case 4: return launch_bt<HD, 4>(split, bt, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
+    case 8: return launch_bt<HD, 8>(split, bt, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -780,8 +819,10 @@ int prefix_prefill(const void* q, int64_t q_row_stride, void* o, int total_q_tok
                    int n_q_heads, const void* kv_pool, int64_t num_pool_blocks, int block_tokens,
                    int n_layers, int n_kv_heads, int head_dim, int layer, const int* req_meta,
                    const int* blk_ids, const int* blk_valid, const int* blk_pos, const int* work,
-                   int n_work, float softmax_scale, const void* rope_table, cudaStream_t stream) {
+                   int n_work, float softmax_scale, const void* rope_table, int work_flags,
+                   cudaStream_t stream) {
   if (n_work == 0) return RCB_OK;
+  const bool split_only = (work_flags & RCB_WORK_SPLIT_ONLY) != 0;
   if (head_dim != 64 && head_dim != 128) return set_error(RCB_ERR_ARG, "head_dim must be 64 or 128");
   if (n_kv_heads <= 0 || n_q_heads % n_kv_heads != 0) return set_error(RCB_ERR_ARG, "bad head counts");
   const int g = n_q_heads / n_kv_heads;
@@ -810,10 +851,10 @@ int prefix_prefill(const void* q, int64_t q_row_stride, void* o, int total_q_tok
   const float sl2 = softmax_scale * 1.4426950408889634f;
   cudaError_t e =
       head_dim == 128
-          ? attn::launch_g<128>(g, block_tokens, tq, tkv, o, n_q_heads, layer, blk_ids,
+          ? attn::launch_g<128>(split_only, g, block_tokens, tq, tkv, o, n_q_heads, layer, blk_ids,
                                 blk_valid, blk_pos, work, n_work, sl2,
                                 static_cast<const float2*>(rope_table), stream)
-          : attn::launch_g<64>(g, block_tokens, tq, tkv, o, n_q_heads, layer, blk_ids,
+          : attn::launch_g<64>(split_only, g, block_tokens, tq, tkv, o, n_q_heads, layer, blk_ids,
                                blk_valid, blk_pos, work, n_work, sl2,
                                static_cast<const float2*>(rope_table), stream);
   if (e != cudaSuccess) return set_cuda_error(e, "prefix_prefill launch");

@@ -22,7 +22,8 @@ int prefix_prefill(const void* q, int64_t q_row_stride, void* o, int total_q_tok
                    int n_q_heads, const void* kv_pool, int64_t num_pool_blocks, int block_tokens,
                    int n_layers, int n_kv_heads, int head_dim, int layer, const int* req_meta,
                    const int* blk_ids, const int* blk_valid, const int* blk_pos, const int* work,
-                   int n_work, float softmax_scale, const void* rope_table, cudaStream_t stream);
+                   int n_work, float softmax_scale, const void* rope_table, int work_flags,
+                   cudaStream_t stream);
 
 // block copy with the (src, dst) block-index list passed by value in the launch
 constexpr int kPairsPerLaunch = 1024;

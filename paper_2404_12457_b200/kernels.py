@@ -141,6 +141,9 @@ class AttnPlan:
         self.half_q0 = ((packed >> 15) & 1).astype(bool)
         self.half_q1 = ((packed >> 31) & 1).astype(bool)
         self.kv_tiles = int(np.maximum(self.tiles_q0, self.tiles_q1).sum()) if self.n_work else 0
+        # every item a lone query tile (decode, short prompts over cached docs): the kernel
+        # variant with one Q tile per item buffer and a deeper K/V ring
+        self.work_flags = _lib.RCB_WORK_SPLIT_ONLY if not self.tiles_q1.any() else 0
         self.mma_tiles = int((self.tiles_q0 + self.tiles_q1).sum()) if self.n_work else 0
         # work items first: the kernel reads them as int4 (16-byte aligned)
         pack = np.concatenate([work[: self.n_work * 8], meta_np, np.asarray(ids, dtype=np.int32),
@@ -180,7 +183,8 @@ def prefix_prefill(q: torch.Tensor, out: torch.Tensor, plan: AttnPlan, pool_base
         num_pool_blocks, block_tokens, n_layers, n_kv_heads, head_dim, layer,
         _dev_ptr(plan.meta), _dev_ptr(plan.blk_ids), _dev_ptr(plan.blk_valid),
         _dev_ptr(plan.blk_pos), _dev_ptr(plan.work), plan.n_work, float(softmax_scale),
-        _dev_ptr(rope) if rope is not None else None, _stream(stream)), "rcb_prefix_prefill")
+        _dev_ptr(rope) if rope is not None else None, plan.work_flags, _stream(stream)),
+        "rcb_prefix_prefill")
 
 
 class RetrievalWorkspace:

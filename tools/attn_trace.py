@@ -31,7 +31,7 @@ def main():
     case = os.environ.get("TRACE_CASE", "long")
     hq, hkv, bt, hd, L = 32, 8, 64, 128, 2
     reqs = {"long": [(4096, 256)] * 32, "miss": [(0, 1056)] * 16,
-            "hit": [(1024, 32)] * 64}[case]
+            "hit": [(1024, 32)] * 64, "decode": [(4096, 1)] * 64}[case]
     total_slots = sum(-(-(a + b) // bt) for a, b in reqs)
     nb = total_slots + 8
     pool = (torch.randn((nb, L, 2, hkv, bt, hd), device="cuda") * 0.5).to(torch.bfloat16)
@@ -54,6 +54,9 @@ def main():
     assert fn(buf.ctypes.data, buf.nbytes) == 0
     tr = buf.reshape(TILES, EV).astype(np.float64)
     mine = np.arange(0, plan.n_work, 148)  # CTA 0's items
+    if os.environ.get("TRACE_DUMP"):
+        np.save(os.environ["TRACE_DUMP"], buf.reshape(TILES, EV))
+        print("items", [(int(plan.tiles_q0[i]), int(plan.tiles_q1[i])) for i in mine])
     steps = int(np.maximum(plan.tiles_q0, plan.tiles_q1)[mine].sum())
     n = min(steps, TILES) - 1
     tr = tr[:n]

@@ -116,8 +116,9 @@ def main(tag: str) -> None:
     lpath = os.path.join(OUT, f"{tag}_bench_launches.csv")
     if os.path.exists(lpath):
         res["launches"] = launch_shares(lpath)
-    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    json.dump(res, open(os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.json"), "w"), indent=1)
+    prof = os.environ.get("PROFILES_DIR", os.path.join(ROOT, "profiles"))  # gpurun: gpurun_out
+    os.makedirs(prof, exist_ok=True)
+    json.dump(res, open(os.path.join(prof, f"{tag}_ncu_summary.json"), "w"), indent=1)
     lines = [f"# ncu summary ({tag})", "",
              "Captures: `ncu --set full --clock-control none --import-source on` (one launch each, "
              "tools/ncu_capture.sh); numbers taken under ncu are profiles, not bench values.", "",
@@ -137,7 +138,7 @@ def main(tag: str) -> None:
         for r in res["launches"][:12]:
             lines.append(f"| `{r['kernel'][:70]}` | {r['launches']} | {r['total_ms']:.2f} | "
                          f"{100 * r['share']:.1f}% |")
-    open(os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.md"), "w").write("\n".join(lines) + "\n")
+    open(os.path.join(prof, f"{tag}_ncu_summary.md"), "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
 

@@ -49,7 +49,7 @@ constexpr int kPolyCols = RCB_POLY_COLS;
 // Per-step handoff timestamps of CTA 0 (debug builds with -DRCB_TRACE only; tools/attn_trace.py)
 //   softmax WG w, its tile c: [c][4w + 0] S wait start, [4w + 1] S seen, [4w + 2] P arrive
 //   MMA, step s: [s][8] P0 seen, [9] QK0 issued, [10] P1 seen, [11] QK1 issued,
-//   [12] K(s) seen full, [13] PV0 issued, [14] PV1 issued
+//   [12] K(s) seen full, [13] PV0 issued, [14] PV1 issued, [15] Q seen (first step of an item)
 #ifdef RCB_TRACE
 constexpr int kTraceTiles = 1024;
 constexpr int kTraceEv = 16;
@@ -356,8 +356,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           bool k_ready = false;
           auto need_k = [&]() {
             if (k_ready) return;
-            if (j == 0)  // Q landed (and, with fused RoPE, rotated by the epilogue WG)
-            mbar_wait(&bar[(rope != nullptr ? kQReady0 : kQFull0) + qb], (ii >> 1) & 1);
+            if (j == 0) {  // Q landed (and, with fused RoPE, rotated by the epilogue WG)
+              mbar_wait(&bar[(rope != nullptr ? kQReady0 : kQFull0) + qb], (ii >> 1) & 1);
+              TRACE(s, 15);
+            }
             mbar_wait(&kv_full[ku % NS], (ku / NS) & 1);
             TRACE(s, 12);
             tc_fence_after();

@@ -69,3 +69,60 @@ def test_attn_plan_host_logic():
     for p, h0, h1 in zip(w[r1, 5], plan.half_q0[r1], plan.half_q1[r1]):
         assert h0 == ((64 * p + 31) % 128 < 64)
         assert h1 == (((64 * p + 63) % 128 < 64) if 64 * p + 32 < 544 else False)
+
+
+def test_layered_swap_api_accounting_mode():
+    """flush_layered / fence_layer / drain on an accounting pool (no device memory):
+    batches are accounted like rcb_pool_flush, arguments are validated."""
+    import pytest
+
+    from paper_2404_12457_b200.pool import PoolError, accounting_pool
+
+    pool = accounting_pool(32, 16, 16)
+    pool.node_alloc_gpu(1, 40)  # 3 blocks
+    pool.node_swap_out([1])
+    pool.flush_layered(1)  # pending D2H: issued (accounted) as a normal batch
+    assert pool.stats()["d2h_bytes"] == 3 * pool.block_bytes
+    pool.node_swap_in([1])
+    pool.flush_layered(4)  # layers_per_group larger than n_layers is clamped
+    assert pool.stats()["h2d_bytes"] == 3 * pool.block_bytes
+    pool.fence_layer(0, None)
+    pool.drain()
+    with pytest.raises(PoolError):
+        pool.flush_layered(0)
+    with pytest.raises(PoolError):
+        pool.fence_layer(1, None)  # the accounting pool has one layer
+    pool.close()
+
+
+def test_attn_plan_split_only_flag():
+    """Plans whose items are all lone query tiles select the split-only kernel variant."""
+    import numpy as np
+
+    # the host-only part of kernels.AttnPlan: the planner through the C-ABI
+    def work_flags(reqs, g=4):
+        meta, valid, pos = [], [], []
+        q_start = 0
+        for q_len, q_pos0 in reqs:
+            n = -(-(q_pos0 + q_len) // 64)
+            meta += [q_start, q_len, q_pos0, len(valid), n]
+            for b in range(n):
+                valid.append(min(64, q_pos0 + q_len - 64 * b))
+                pos.append(64 * b)
+            q_start += q_len
+        requests = reqs
+        cap = 4096
+        work = np.zeros(cap * 8, dtype=np.int32)
+        n = np.zeros(1, dtype=np.int32)
+        lib = _lib.load()
+        assert lib.rcb_attn_plan(np.asarray(meta, np.int32).ctypes.data_as(_lib._p32), len(requests),
+                                 np.asarray(valid, np.int32).ctypes.data_as(_lib._p32),
+                                 np.asarray(pos, np.int32).ctypes.data_as(_lib._p32), 64, 8 * g, 8,
+                                 work.ctypes.data_as(_lib._p32), cap,
+                                 n.ctypes.data_as(_lib._p32)) == 0
+        tiles_q1 = (work[: n[0] * 8].reshape(-1, 8)[:, 7].view(np.uint32) >> 16) & 0x7FFF
+        return 0 if tiles_q1.any() else _lib.RCB_WORK_SPLIT_ONLY
+
+    assert work_flags([(1, 4096)] * 8) == _lib.RCB_WORK_SPLIT_ONLY      # decode
+    assert work_flags([(32, 1024)] * 8) == _lib.RCB_WORK_SPLIT_ONLY     # full hits, 32-token prompt
+    assert work_flags([(1056, 0)] * 2) == 0                              # misses: tile pairs

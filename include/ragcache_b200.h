@@ -187,6 +187,16 @@ int rcb_attn_plan(const int32_t* req_meta, int32_t n_req, const int32_t* blk_val
                   const int32_t* blk_pos, int32_t block_tokens, int32_t n_q_heads,
                   int32_t n_kv_heads, int32_t* work_out, int32_t cap, int32_t* n_work_out);
 
+/* fused elementwise ops of the random-init decoder whose measured prefill and decode
+ * step replace ragsim's T(alpha, beta) grid and decode_ms_per_token (cost_model.py:40-67,
+ * config.py:52; paper_2404_12457_b200/profile.py).  fp32 residual stream x [n_rows][d]:
+ * x += add (bf16, NULL = none); h_out = bf16(x * rsqrt(mean(x^2) + eps) * weight). */
+int rcb_rmsnorm_residual(float* x_dev, const void* add_dev, const void* weight_dev,
+                         void* h_out_dev, int32_t n_rows, int32_t d, float eps, void* stream);
+/* out [n_rows][ffn] = bf16(silu(gate) * up), gate_up [n_rows][2*ffn] = (gate | up) */
+int rcb_silu_mul(const void* gate_up_dev, void* out_dev, int32_t n_rows, int32_t ffn,
+                 void* stream);
+
 /* (3) exact inner-product top-k retrieval, staged (tcgen05 corpus GEMM +
  * top-k epilogue).  Stand-in replaced: generate_stages / StagedRetrieval
  * (speculation.py:33-59,149-194) behind the StageProvider seam (simulator.py:228).

@@ -90,6 +90,9 @@ SIGNATURES = [
                                    c_int64, c_int32, c_int32, c_int32, c_int32, c_int32,
                                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32,
                                    c_float, c_void_p, c_int32, c_void_p]),
+    ("rcb_rmsnorm_residual", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32,
+                                     c_float, c_void_p]),
+    ("rcb_silu_mul", c_int, [c_void_p, c_void_p, c_int32, c_int32, c_void_p]),
     ("rcb_attn_plan", c_int, [_p32, c_int32, _p32, _p32, c_int32, c_int32, c_int32, _p32,
                               c_int32, _p32]),
     ("rcb_retrieval_workspace_bytes", c_int64, [c_int64, c_int32, c_int32, c_int32]),

@@ -187,6 +187,30 @@ def prefix_prefill(q: torch.Tensor, out: torch.Tensor, plan: AttnPlan, pool_base
         "rcb_prefix_prefill")
 
 
+def rmsnorm_residual(x: torch.Tensor, add: torch.Tensor | None, weight: torch.Tensor,
+                     eps: float, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """x (fp32 [T, d], updated in place) += add (bf16); returns bf16 rmsnorm(x) * weight."""
+    assert x.dtype == torch.float32 and x.is_contiguous() and weight.dtype == torch.bfloat16
+    if add is not None:
+        assert add.dtype == torch.bfloat16 and add.is_contiguous() and add.shape == x.shape
+    if out is None:
+        out = torch.empty(x.shape, dtype=torch.bfloat16, device=x.device)
+    check(load().rcb_rmsnorm_residual(
+        _dev_ptr(x), _dev_ptr(add) if add is not None else None, _dev_ptr(weight), _dev_ptr(out),
+        x.shape[0], x.shape[1], float(eps), _stream(stream)), "rcb_rmsnorm_residual")
+    return out
+
+
+def silu_mul(gate_up: torch.Tensor, stream=None) -> torch.Tensor:
+    """gate_up bf16 [T, 2F] -> bf16 silu(gate) * up [T, F]."""
+    assert gate_up.dtype == torch.bfloat16 and gate_up.is_contiguous()
+    t, f2 = gate_up.shape
+    out = torch.empty((t, f2 // 2), dtype=torch.bfloat16, device=gate_up.device)
+    check(load().rcb_silu_mul(_dev_ptr(gate_up), _dev_ptr(out), t, f2 // 2, _stream(stream)),
+          "rcb_silu_mul")
+    return out
+
+
 class RetrievalWorkspace:
     def __init__(self, n_rows: int, n_queries: int, k: int, n_stages: int, device="cuda"):
         self.nbytes = int(load().rcb_retrieval_workspace_bytes(n_rows, n_queries, k, n_stages))

@@ -71,11 +71,6 @@ def init_weights(dims: ModelDims, seed: int = 0, device="cuda", dtype=torch.bflo
     }
 
 
-def rms_norm(x: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
-    xf = x.float()
-    return xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps) * w.float()
-
-
 class PrefillModel:
     def __init__(self, dims: ModelDims, weights, *, block_tokens: int, num_pool_blocks: int,
                  pool_base: int) -> None:
@@ -103,8 +98,11 @@ class PrefillModel:
         attn = torch.empty((T, s.n_q_heads, s.head_dim), dtype=bf, device=x.device)
         qw = s.n_q_heads * s.head_dim
         kw = s.n_kv_heads * s.head_dim
-        for layer, lw in enumerate(self.w["layers"]):
-            h = rms_norm(x, lw["ln1"], d.norm_eps).to(bf)
+        layers = self.w["layers"]
+        # residual add + RMSNorm and SiLU * up run as one kernel each (rcb_rmsnorm_residual,
+        # rcb_silu_mul); the projections are library GEMMs
+        h = kernels.rmsnorm_residual(x, None, layers[0]["ln1"], d.norm_eps, stream=stream)
+        for layer, lw in enumerate(layers):
             qkv = h @ lw["wqkv"]
             # K/V rotated into the pool; Q's RoPE runs inside the attention kernel
             kernels.kv_write_rope(None, qkv[:, qw:qw + kw], qkv[:, qw + kw:], None, positions,
@@ -117,13 +115,12 @@ class PrefillModel:
                                    block_tokens=self.bt, n_layers=s.n_layers,
                                    n_kv_heads=s.n_kv_heads, head_dim=s.head_dim, layer=layer,
                                    rope=self.rope, n_q_heads=s.n_q_heads, stream=stream)
-            x = x + (attn.view(T, qw) @ lw["wo"]).float()
-            h = rms_norm(x, lw["ln2"], d.norm_eps).to(bf)
-            gu = h @ lw["wgu"]
-            gate, up = gu[:, : d.ffn], gu[:, d.ffn:]
-            x = x + ((torch.nn.functional.silu(gate.float()) * up.float()).to(bf) @ lw["wdown"]).float()
-        h = rms_norm(x[last_rows], self.w["norm"], d.norm_eps).to(bf)
-        return (h @ self.w["lm_head"]).float()
+            h = kernels.rmsnorm_residual(x, attn.view(T, qw) @ lw["wo"], lw["ln2"], d.norm_eps,
+                                         stream=stream)
+            mlp = kernels.silu_mul(h @ lw["wgu"], stream=stream) @ lw["wdown"]
+            nxt = layers[layer + 1]["ln1"] if layer + 1 < len(layers) else self.w["norm"]
+            h = kernels.rmsnorm_residual(x, mlp, nxt, d.norm_eps, stream=stream)
+        return (h[last_rows] @ self.w["lm_head"]).float()
 
 
 def suffix_slots(blocks, valid, n_prefix_blocks: int, block_tokens: int, alpha: int):

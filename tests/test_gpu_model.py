@@ -76,3 +76,23 @@ def test_cached_prefix_prefill_matches_full_recompute():
     assert mag > 0.1  # logits are not trivially small
     errs = (err_a, err_b, err_c)
     assert max(errs) <= LOGIT_ATOL, f"max |logit err| per request {errs} (max |logit| {mag:.3f})"
+
+
+@pytest.mark.parametrize("t,d", [(1, 4096), (37, 256), (300, 5120)])
+def test_fused_rmsnorm_residual_and_silu_mul(t, d):
+    """rcb_rmsnorm_residual / rcb_silu_mul vs the fp32 torch expressions they replace
+    (model.py before the fusion): residual exact in fp32, outputs within one bf16 ulp."""
+    g = torch.Generator(device="cpu").manual_seed(t)
+    x = torch.randn((t, d), generator=g).cuda()
+    add = torch.randn((t, d), generator=g).cuda().to(torch.bfloat16)
+    w = (1 + 0.1 * torch.randn(d, generator=g)).cuda().to(torch.bfloat16)
+    x_ref = x + add.float()
+    h_ref = (x_ref * torch.rsqrt(x_ref.pow(2).mean(-1, keepdim=True) + 1e-5) * w.float())
+    h = kernels.rmsnorm_residual(x, add, w, 1e-5)
+    torch.cuda.synchronize()
+    assert torch.equal(x, x_ref)
+    assert (h.float() - h_ref).abs().max().item() <= 1e-2 * h_ref.abs().max().item()
+    gu = torch.randn((t, 2 * d), generator=g).cuda().to(torch.bfloat16)
+    a_ref = torch.nn.functional.silu(gu[:, :d].float()) * gu[:, d:].float()
+    a = kernels.silu_mul(gu)
+    assert (a.float() - a_ref).abs().max().item() <= 1e-2 * a_ref.abs().max().item()

@@ -170,7 +170,13 @@ int rcb_rope_table(void* table_dev, int32_t max_pos, int32_t head_dim, float rop
  *                 rcb_attn_plan, heaviest first)
  *   work_flags  : RCB_WORK_SPLIT_ONLY if every item has n1 == 0 (one query tile: decode
  *                 steps, short prompts over cached documents); the kernel then keeps one
- *                 Q tile per item buffer and runs a deeper K/V ring (HBM-bound launches) */
+ *                 Q tile per item buffer and runs a deeper K/V ring (HBM-bound launches)
+ *   split-KV (split-only plans with few items, e.g. one request's decode step): items whose
+ *                 field 6 is kv_head | (slot + 1) << 8 cover part of a query tile's KV range
+ *                 and write fp32 (O, max, sum) to part slot `slot` of part_ws_dev =
+ *                 float2 [n_part_slots][128] then float [n_part_slots][128][head_dim];
+ *                 combine_dev = int32 [n_combine][6] {q_start, q_len, tok_base, kv_head,
+ *                 slot0, n_parts} merges them into o.  NULL / 0 when unused. */
 #define RCB_WORK_SPLIT_ONLY 1
 int rcb_prefix_prefill(const void* q, int64_t q_row_stride, void* o, int32_t total_q_tokens,
                        int32_t n_q_heads, const void* kv_pool, int64_t num_pool_blocks,
@@ -179,7 +185,8 @@ int rcb_prefix_prefill(const void* q, int64_t q_row_stride, void* o, int32_t tot
                        const int32_t* blk_ids_dev, const int32_t* blk_valid_dev,
                        const int32_t* blk_pos_dev, const int32_t* work_dev, int32_t n_work,
                        float softmax_scale, const void* rope_table_dev, int32_t work_flags,
-                       void* stream);
+                       void* part_ws_dev, int32_t n_part_slots, const int32_t* combine_dev,
+                       int32_t n_combine, void* stream);
 /* host-side work planner for rcb_prefix_prefill: writes up to cap items (8 int32 each) into
  * work_out (heaviest first) and returns the count in n_work_out.  Inputs are the
  * host copies of req_meta / blk_valid / blk_pos. */

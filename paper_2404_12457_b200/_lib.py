@@ -89,7 +89,8 @@ SIGNATURES = [
     ("rcb_prefix_prefill", c_int, [c_void_p, c_int64, c_void_p, c_int32, c_int32, c_void_p,
                                    c_int64, c_int32, c_int32, c_int32, c_int32, c_int32,
                                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32,
-                                   c_float, c_void_p, c_int32, c_void_p]),
+                                   c_float, c_void_p, c_int32, c_void_p, c_int32, c_void_p,
+                                   c_int32, c_void_p]),
     ("rcb_rmsnorm_residual", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32,
                                      c_float, c_void_p]),
     ("rcb_silu_mul", c_int, [c_void_p, c_void_p, c_int32, c_int32, c_void_p]),

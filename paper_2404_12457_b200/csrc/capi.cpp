@@ -73,13 +73,15 @@ int rcb_prefix_prefill(const void* q, int64_t q_row_stride, void* o, int32_t tot
                        const int32_t* blk_ids_dev, const int32_t* blk_valid_dev,
                        const int32_t* blk_pos_dev, const int32_t* work_dev, int32_t n_work,
                        float softmax_scale, const void* rope_table_dev, int32_t work_flags,
-                       void* stream) {
+                       void* part_ws_dev, int32_t n_part_slots, const int32_t* combine_dev,
+                       int32_t n_combine, void* stream) {
   if (block_tokens != 16 && block_tokens != 32 && block_tokens != 64 && block_tokens != 128)
     return rcb::set_error(RCB_ERR_ARG, "block_tokens must be 16, 32, 64 or 128");
   return rcb::prefix_prefill(q, q_row_stride, o, total_q_tokens, n_q_heads, kv_pool,
                              num_pool_blocks, block_tokens, n_layers, n_kv_heads, head_dim, layer,
                              req_meta_dev, blk_ids_dev, blk_valid_dev, blk_pos_dev, work_dev,
-                             n_work, softmax_scale, rope_table_dev, work_flags,
+                             n_work, softmax_scale, rope_table_dev, work_flags, part_ws_dev,
+                             n_part_slots, combine_dev, n_combine,
                              static_cast<cudaStream_t>(stream));
 }
 

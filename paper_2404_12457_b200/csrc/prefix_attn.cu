@@ -112,6 +112,7 @@ constexpr int kItemInts = 8;
 struct Item {
   int q_start, q_len, q_pos0, blk_begin, blk_count, qp, kvh, n0, n1;
   bool h0, h1;
+  int ps;  // split-KV part slot (-1: the item writes bf16 O directly)
   __device__ __forceinline__ bool split() const { return n1 == 0; }
   __device__ __forceinline__ int n() const { return n0 > n1 ? n0 : n1; }
   // WG w works on step j
@@ -139,8 +140,10 @@ __device__ __forceinline__ Item load_item(const int* __restrict__ work, int idx)
   const int4 a = *reinterpret_cast<const int4*>(work + idx * kItemInts);
   const int4 b = *reinterpret_cast<const int4*>(work + idx * kItemInts + 4);
   const uint32_t p = static_cast<uint32_t>(b.w);
-  return Item{a.x, a.y, a.z, a.w, b.x, b.y, b.z, static_cast<int>(p & 0x7fffu),
-              static_cast<int>((p >> 16) & 0x7fffu), ((p >> 15) & 1u) != 0, (p >> 31) != 0};
+  // field 6 = kv_head | (split-KV part slot + 1) << 8
+  return Item{a.x, a.y, a.z, a.w, b.x, b.y, b.z & 0xff, static_cast<int>(p & 0x7fffu),
+              static_cast<int>((p >> 16) & 0x7fffu), ((p >> 15) & 1u) != 0, (p >> 31) != 0,
+              (b.z >> 8) - 1};
 }
 
 // Persistent: CTA c serves work items c, c + grid, ... (heaviest first).  The KV step
@@ -154,7 +157,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                           __nv_bfloat16* __restrict__ out, int n_q_heads, int layer,
                           const int* __restrict__ blk_ids, const int* __restrict__ blk_valid,
                           const int* __restrict__ blk_pos, const int* __restrict__ work,
-                          int n_work, float scale_log2, const float2* __restrict__ rope) {
+                          int n_work, float scale_log2, const float2* __restrict__ rope,
+                          float* __restrict__ part_o, float2* __restrict__ part_ml) {
   using S = Smem<HD, BT, SPLIT>;
   constexpr int TQ = kRows / G;  // tokens per query tile
   constexpr int BPT = S::kBPT;
@@ -686,6 +690,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
       c0 *= inv_l;
       c1 *= inv_l;
+      // split-KV part (split-only launches): normalised fp32 O and (max, sum) of this KV
+      // range go to the part workspace; rcb attn_combine_kernel merges the parts
+      const bool part = SPLIT && it.ps >= 0;
+      if (part && row_valid) part_ml[static_cast<int64_t>(it.ps) * kRows + row] = make_float2(mm, l);
       if (use0) mbar_wait(&bar[kOFull0 + 0], oc[0] & 1);
       if (use1) mbar_wait(&bar[kOFull0 + 1], oc[1] & 1);
       tc_fence_after();
@@ -712,7 +720,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         // are 256 B apart, so every store touches 32 lines; with 16-byte stores the O
         // drain doubled those wavefronts and its LSU traffic stalled the softmax warps
         // sharing the SM sub-partitions (trace: -18% cycles per KV step without it)
-        if (row_valid) {
+        if (part) {
+          if (!row_valid) continue;  // rows past q_len: nothing to combine
+          float* prow = part_o + (static_cast<int64_t>(it.ps) * kRows + row) * HD + ch * 32;
+#pragma unroll
+          for (int i = 0; i < 32; i += 8)
+            asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
+                         :: "l"(prow + i), "f"(o[i]), "f"(o[i + 1]), "f"(o[i + 2]), "f"(o[i + 3]),
+                            "f"(o[i + 4]), "f"(o[i + 5]), "f"(o[i + 6]), "f"(o[i + 7])
+                         : "memory");
+        } else if (row_valid) {
 #pragma unroll
           for (int i = 0; i < 32; i += 16) {
             uint32_t v[8];
@@ -756,11 +773,58 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// Split-KV combine: group = {q_start, q_len, tok_base, kv_head, slot0, n_parts} of one
+// query tile whose KV range ran as n_parts items.  Thread = tile row (token, head);
+// O = sum_p 2^(m_p - M) l_p O_p / sum_p 2^(m_p - M) l_p over parts with l_p > 0.
+constexpr int kGroupInts = 6;
+__global__ void __launch_bounds__(kRows)
+    attn_combine_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml,
+                        const int* __restrict__ groups, __nv_bfloat16* __restrict__ out,
+                        int n_q_heads, int G, int HD) {
+  const int* gp = groups + blockIdx.x * kGroupInts;
+  const int q_start = gp[0], q_len = gp[1], tok_base = gp[2], kvh = gp[3], slot0 = gp[4],
+            np = gp[5];
+  const int row = threadIdx.x;
+  const int tok = tok_base + row / G;
+  if (tok >= q_len) return;
+  float mx = -INFINITY;
+  for (int p = 0; p < np; ++p) {
+    const float2 ml = part_ml[static_cast<int64_t>(slot0 + p) * kRows + row];
+    if (ml.y > 0.f) mx = fmaxf(mx, ml.x);
+  }
+  float wsum = 0.f;
+  float wt[32];
+  for (int p = 0; p < np && p < 32; ++p) {
+    const float2 ml = part_ml[static_cast<int64_t>(slot0 + p) * kRows + row];
+    wt[p] = ml.y > 0.f ? exp2f(ml.x - mx) * ml.y : 0.f;
+    wsum += wt[p];
+  }
+  const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+  __nv_bfloat16* orow = out + (static_cast<int64_t>(q_start + tok) * n_q_heads + kvh * G + row % G) * HD;
+  for (int c = 0; c < HD; c += 8) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int p = 0; p < np && p < 32; ++p) {
+      const float4* src = reinterpret_cast<const float4*>(
+          part_o + (static_cast<int64_t>(slot0 + p) * kRows + row) * HD + c);
+      const float4 a = src[0], b = src[1];
+      const float w = wt[p] * inv;
+      acc[0] += w * a.x; acc[1] += w * a.y; acc[2] += w * a.z; acc[3] += w * a.w;
+      acc[4] += w * b.x; acc[5] += w * b.y; acc[6] += w * b.z; acc[7] += w * b.w;
+    }
+    uint4 v;
+    v.x = pack_bf16(acc[0], acc[1]);
+    v.y = pack_bf16(acc[2], acc[3]);
+    v.z = pack_bf16(acc[4], acc[5]);
+    v.w = pack_bf16(acc[6], acc[7]);
+    *reinterpret_cast<uint4*>(orow + c) = v;
+  }
+}
+
 template <int HD, int G, int BT, bool SPLIT>
 cudaError_t launch_s(const CUtensorMap& tq, const CUtensorMap& tkv, void* out, int n_q_heads,
                      int layer, const int* blk_ids, const int* blk_valid,
                      const int* blk_pos, const int* work, int n_work, float scale_log2,
-                     const float2* rope, cudaStream_t stream) {
+                     const float2* rope, float* part_o, float2* part_ml, cudaStream_t stream) {
   auto kern = prefix_prefill_kernel<HD, G, BT, SPLIT>;
   const uint32_t smem = Smem<HD, BT, SPLIT>::kTotal;
   static bool attr_set = false;  // per instantiation
@@ -779,7 +843,7 @@ cudaError_t launch_s(const CUtensorMap& tq, const CUtensorMap& tkv, void* out, i
   const int grid = n_work < sms ? n_work : sms;
   kern<<<grid, kThreads, smem, stream>>>(tq, tkv, static_cast<__nv_bfloat16*>(out), n_q_heads,
                                         layer, blk_ids, blk_valid, blk_pos, work, n_work,
-                                        scale_log2, rope);
+                                        scale_log2, rope, part_o, part_ml);
   return cudaGetLastError();
 }
 
@@ -787,21 +851,21 @@ template <int HD, int G, int BT>
 cudaError_t launch_t(bool split, const CUtensorMap& tq, const CUtensorMap& tkv, void* out,
                      int n_q_heads, int layer, const int* bi, const int* bv, const int* bp,
                      const int* work, int n_work, float sl2, const float2* rope,
-                     cudaStream_t st) {
-  return split ? launch_s<HD, G, BT, true>(tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st)
-               : launch_s<HD, G, BT, false>(tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
+                     float* po, float2* pm, cudaStream_t st) {
+  return split ? launch_s<HD, G, BT, true>(tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st)
+               : launch_s<HD, G, BT, false>(tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
 }
 
 template <int HD, int G>
 cudaError_t launch_bt(bool split, int bt, const CUtensorMap& tq, const CUtensorMap& tkv, void* out,
                       int n_q_heads, int layer, const int* bi, const int* bv,
                       const int* bp, const int* work, int n_work, float sl2, const float2* rope,
-                      cudaStream_t st) {
+                      float* po, float2* pm, cudaStream_t st) {
   switch (bt) {
-    case 16: return launch_t<HD, G, 16>(split, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
-    case 32: return launch_t<HD, G, 32>(split, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
-    case 64: return launch_t<HD, G, 64>(split, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
-    case 128: return launch_t<HD, G, 128>(split, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
+    case 16: return launch_t<HD, G, 16>(split, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
+    case 32: return launch_t<HD, G, 32>(split, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
+    case 64: return launch_t<HD, G, 64>(split, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
+    case 128: return launch_t<HD, G, 128>(split, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -810,12 +874,12 @@ template <int HD>
 cudaError_t launch_g(bool split, int g, int bt, const CUtensorMap& tq, const CUtensorMap& tkv, void* out,
                      int n_q_heads, int layer, const int* bi, const int* bv,
                      const int* bp, const int* work, int n_work, float sl2, const float2* rope,
-                     cudaStream_t st) {
+                     float* po, float2* pm, cudaStream_t st) {
   switch (g) {
-    case 1: return launch_bt<HD, 1>(split, bt, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
-    case 2: return launch_bt<HD, 2>(split, bt, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
-    case 4: return launch_bt<HD, 4>(split, bt, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
-    case 8: return launch_bt<HD, 8>(split, bt, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, st);
+    case 1: return launch_bt<HD, 1>(split, bt, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
+    case 2: return launch_bt<HD, 2>(split, bt, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
+    case 4: return launch_bt<HD, 4>(split, bt, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
+    case 8: return launch_bt<HD, 8>(split, bt, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -827,11 +891,19 @@ int prefix_prefill(const void* q, int64_t q_row_stride, void* o, int total_q_tok
                    int n_layers, int n_kv_heads, int head_dim, int layer, const int* req_meta,
                    const int* blk_ids, const int* blk_valid, const int* blk_pos, const int* work,
                    int n_work, float softmax_scale, const void* rope_table, int work_flags,
+                   void* part_ws, int n_part_slots, const int* combine, int n_combine,
                    cudaStream_t stream) {
   if (n_work == 0) return RCB_OK;
   if (reinterpret_cast<uintptr_t>(o) % 32 != 0)
     return set_error(RCB_ERR_ARG, "attention output must be 32-byte aligned");
   const bool split_only = (work_flags & RCB_WORK_SPLIT_ONLY) != 0;
+  if (n_combine > 0 && (!split_only || part_ws == nullptr || combine == nullptr || n_part_slots <= 0))
+    return set_error(RCB_ERR_ARG, "split-KV parts need a split-only plan and a part workspace");
+  // part workspace: float2 (max, sum) [slots][128 rows], then fp32 O [slots][128 rows][head_dim]
+  float2* part_ml = static_cast<float2*>(part_ws);
+  float* part_o = part_ws != nullptr
+                      ? reinterpret_cast<float*>(part_ml + static_cast<int64_t>(n_part_slots) * 128)
+                      : nullptr;
   if (head_dim != 64 && head_dim != 128) return set_error(RCB_ERR_ARG, "head_dim must be 64 or 128");
   if (n_kv_heads <= 0 || n_q_heads % n_kv_heads != 0) return set_error(RCB_ERR_ARG, "bad head counts");
   const int g = n_q_heads / n_kv_heads;
@@ -862,11 +934,17 @@ int prefix_prefill(const void* q, int64_t q_row_stride, void* o, int total_q_tok
       head_dim == 128
           ? attn::launch_g<128>(split_only, g, block_tokens, tq, tkv, o, n_q_heads, layer, blk_ids,
                                 blk_valid, blk_pos, work, n_work, sl2,
-                                static_cast<const float2*>(rope_table), stream)
+                                static_cast<const float2*>(rope_table), part_o, part_ml, stream)
           : attn::launch_g<64>(split_only, g, block_tokens, tq, tkv, o, n_q_heads, layer, blk_ids,
                                blk_valid, blk_pos, work, n_work, sl2,
-                               static_cast<const float2*>(rope_table), stream);
+                               static_cast<const float2*>(rope_table), part_o, part_ml, stream);
   if (e != cudaSuccess) return set_cuda_error(e, "prefix_prefill launch");
+  if (n_combine > 0) {
+    attn::attn_combine_kernel<<<n_combine, attn::kRows, 0, stream>>>(
+        part_o, part_ml, combine, static_cast<__nv_bfloat16*>(o), n_q_heads, g, head_dim);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return set_cuda_error(e, "attention combine launch");
+  }
   return RCB_OK;
 }
 

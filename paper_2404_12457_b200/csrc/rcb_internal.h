@@ -23,6 +23,7 @@ int prefix_prefill(const void* q, int64_t q_row_stride, void* o, int total_q_tok
                    int n_layers, int n_kv_heads, int head_dim, int layer, const int* req_meta,
                    const int* blk_ids, const int* blk_valid, const int* blk_pos, const int* work,
                    int n_work, float softmax_scale, const void* rope_table, int work_flags,
+                   void* part_ws, int n_part_slots, const int* combine, int n_combine,
                    cudaStream_t stream);
 
 // block copy with the (src, dst) block-index list passed by value in the launch

@@ -8,6 +8,7 @@ missing library raises RcbUnavailable, a non-CUDA tensor raises ValueError.
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 import torch
@@ -89,6 +90,48 @@ def kv_write_rope(q, k: torch.Tensor, v: torch.Tensor, q_out, positions: torch.T
         "rcb_kv_write_rope")
 
 
+def _num_sms(device) -> int:
+    try:
+        return torch.cuda.get_device_properties(torch.device(device)).multi_processor_count
+    except (RuntimeError, AssertionError, ValueError):
+        return 148
+
+
+def _split_kv(items: np.ndarray, n_sms: int, bpt: int, tq: int):
+    """Split-KV for split-only plans with few items (one request's decode step or
+    cached-prefix prefill: one item per KV head would leave most SMs idle).  Opt-in:
+    on B200 a single Mistral-7B request measured 27.6 us split vs 18.4 us unsplit (decode,
+    1056-token context) -- the per-CTA prologue and the combine launch outweigh the
+    parallelism at these sizes.  Each item's
+    KV tiles are cut into P contiguous parts (>= 2 tiles, so both softmax warpgroups
+    work); a part writes fp32 (O, max, sum) to its slot and one combine group per split
+    item merges them (rcb_prefix_prefill combine_dev).  Returns (items, groups)."""
+    target = max(1, n_sms // len(items))
+    out, groups, slot = [], [], 0
+    for it in items:
+        packed = int(np.uint32(it[7]))
+        n0, half0 = packed & 0x7FFF, (packed >> 15) & 1
+        parts = max(1, min(target, n0 // 2))
+        if parts == 1:
+            out.append(it.copy())
+            continue
+        cuts = [round(k * n0 / parts) for k in range(parts + 1)]
+        for k in range(parts):
+            t0, t1 = cuts[k], cuts[k + 1]
+            sub = it.copy()
+            sub[3] = it[3] + t0 * bpt
+            sub[4] = min(int(it[4]) - t0 * bpt, (t1 - t0) * bpt)
+            sub[6] = int(it[6]) | ((slot + k + 1) << 8)
+            sub[7] = np.uint32((t1 - t0) | ((half0 if t1 == n0 else 0) << 15)).view(np.int32)
+            out.append(sub)
+        # {q_start, q_len, tok_base, kv_head, slot0, n_parts}
+        groups.append([it[0], it[1], 2 * it[5] * tq, it[6], slot, parts])
+        slot += parts
+    items = np.stack(out).astype(np.int32)
+    order = np.argsort(-(items[:, 7].view(np.uint32) & 0x7FFF), kind="stable")  # heaviest first
+    return items[order], np.asarray(groups, dtype=np.int32).reshape(-1, 6)
+
+
 class AttnPlan:
     """Device-resident block tables + work list for one prefill batch.
 
@@ -98,7 +141,7 @@ class AttnPlan:
     """
 
     def __init__(self, requests, *, block_tokens: int, n_q_heads: int, n_kv_heads: int,
-                 device="cuda") -> None:
+                 device="cuda", split_kv: bool | None = None) -> None:
         meta = []
         ids: list[int] = []
         valid: list[int] = []
@@ -145,9 +188,19 @@ class AttnPlan:
         # variant with one Q tile per item buffer and a deeper K/V ring
         self.work_flags = _lib.RCB_WORK_SPLIT_ONLY if not self.tiles_q1.any() else 0
         self.mma_tiles = int((self.tiles_q0 + self.tiles_q1).sum()) if self.n_work else 0
+        items = work[: self.n_work * 8].reshape(-1, 8)
+        groups = np.zeros((0, 6), dtype=np.int32)
+        self.n_part_slots = 0
+        if split_kv is None:  # opt-in: measured slower at the sizes it targets
+            split_kv = bool(os.environ.get("RCB_SPLIT_KV"))
+        if split_kv and self.work_flags and 0 < self.n_work and 2 * self.n_work <= _num_sms(device):
+            items, groups = _split_kv(items, _num_sms(device), 128 // block_tokens, 128 // g)
+            self.n_part_slots = int(groups[:, 5].sum()) if len(groups) else 0
+        self.n_work = items.shape[0]
+        self.n_combine = groups.shape[0]
         # work items first: the kernel reads them as int4 (16-byte aligned)
-        pack = np.concatenate([work[: self.n_work * 8], meta_np, np.asarray(ids, dtype=np.int32),
-                               valid_np, pos_np])
+        pack = np.concatenate([items.reshape(-1), meta_np, np.asarray(ids, dtype=np.int32),
+                               valid_np, pos_np, groups.reshape(-1)])
         self._buf = _upload(pack, device)
         o = 0
         self.work = self._buf[o:o + self.n_work * 8]; o += self.n_work * 8
@@ -155,7 +208,16 @@ class AttnPlan:
         self.blk_ids = self._buf[o:o + len(ids)]; o += len(ids)
         self.blk_valid = self._buf[o:o + len(ids)]; o += len(ids)
         self.blk_pos = self._buf[o:o + len(ids)]; o += len(ids)
+        self.combine = self._buf[o:o + groups.size]
+        self.part_ws = None  # fp32 split-KV parts, sized on first use (needs head_dim)
         self.requests = requests
+
+
+def _part_ws(plan: AttnPlan, head_dim: int, device) -> torch.Tensor:
+    need = plan.n_part_slots * 128 * (8 + 4 * head_dim)
+    if plan.part_ws is None or plan.part_ws.numel() < need:
+        plan.part_ws = torch.empty(need, dtype=torch.uint8, device=device)
+    return plan.part_ws
 
 
 def prefix_prefill(q: torch.Tensor, out: torch.Tensor, plan: AttnPlan, pool_base: int,
@@ -183,8 +245,10 @@ def prefix_prefill(q: torch.Tensor, out: torch.Tensor, plan: AttnPlan, pool_base
         num_pool_blocks, block_tokens, n_layers, n_kv_heads, head_dim, layer,
         _dev_ptr(plan.meta), _dev_ptr(plan.blk_ids), _dev_ptr(plan.blk_valid),
         _dev_ptr(plan.blk_pos), _dev_ptr(plan.work), plan.n_work, float(softmax_scale),
-        _dev_ptr(rope) if rope is not None else None, plan.work_flags, _stream(stream)),
-        "rcb_prefix_prefill")
+        _dev_ptr(rope) if rope is not None else None, plan.work_flags,
+        _dev_ptr(_part_ws(plan, head_dim, out.device)) if plan.n_part_slots else None,
+        plan.n_part_slots, _dev_ptr(plan.combine) if plan.n_combine else None, plan.n_combine,
+        _stream(stream)), "rcb_prefix_prefill")
 
 
 def rmsnorm_residual(x: torch.Tensor, add: torch.Tensor | None, weight: torch.Tensor,

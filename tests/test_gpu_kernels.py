@@ -15,7 +15,7 @@ import pytest
 import torch
 
 from oracle import attn_oracle, topk_oracle
-from paper_2404_12457_b200 import kernels, synth
+from paper_2404_12457_b200 import _lib, kernels, synth
 
 pytestmark = pytest.mark.gpu
 
@@ -171,11 +171,19 @@ ATTN_CASES = [
     (64, 8, 4, 128, 1, [([129, 3], [260])]),
     # decode steps (one new token per request over its cached context): split items
     (128, 32, 8, 64, 1, [([512, 512], [1]), ([300], [1]), ([512, 512, 512, 512], [1])]),
+    # split-KV (split-only plans with few items): one request's decode step, a cached-prefix
+    # prompt whose causal diagonal crosses a KV tile (fully masked rows in the last part),
+    # MHA, head_dim 64 with 16-token blocks
+    (128, 32, 8, 64, 1, [([4096], [1])]),
+    (128, 32, 8, 64, 1, [([1020], [32])]),
+    (128, 32, 32, 64, 1, [([2048], [1]), ([500], [3])]),
+    (64, 8, 4, 16, 2, [([300, 200], [2])]),
 ]
 
 
+@pytest.mark.parametrize("split_kv", [False, True])
 @pytest.mark.parametrize("hd,hq,hkv,bt,L,reqs", ATTN_CASES)
-def test_prefix_prefill_matches_oracle(hd, hq, hkv, bt, L, reqs):
+def test_prefix_prefill_matches_oracle(hd, hq, hkv, bt, L, reqs, split_kv):
     nb = 400
     pool = _pool(nb, L, hkv, bt, hd, seed=hd + hq + bt)
     free = list(np.random.default_rng(bt).permutation(nb))
@@ -189,7 +197,8 @@ def test_prefix_prefill_matches_oracle(hd, hq, hkv, bt, L, reqs):
     g.manual_seed(7)
     q = torch.randn((total_q, hq, hd), generator=g, device="cuda").to(torch.bfloat16)
     out = torch.zeros_like(q)
-    plan = kernels.AttnPlan(requests, block_tokens=bt, n_q_heads=hq, n_kv_heads=hkv)
+    plan = kernels.AttnPlan(requests, block_tokens=bt, n_q_heads=hq, n_kv_heads=hkv,
+                            split_kv=split_kv)
     for layer in range(L):
         kernels.prefix_prefill(q, out, plan, pool.data_ptr(), nb, block_tokens=bt, n_layers=L,
                                n_kv_heads=hkv, head_dim=hd, layer=layer)
@@ -197,6 +206,16 @@ def test_prefix_prefill_matches_oracle(hd, hq, hkv, bt, L, reqs):
         ref = attn_oracle.prefix_prefill(q.cpu().float(), pool.cpu(), requests, layer)
         err = (out.cpu().float() - ref).abs().max().item()
         assert err <= ATTN_ATOL, f"layer {layer}: max |err| {err}"
+
+
+def test_split_kv_plan_splits_small_split_only_launches():
+    bt = 64
+    free = list(range(200))
+    blocks, valid = _table([4096, 1], bt, free)
+    plan = kernels.AttnPlan([(1, 4096, blocks, valid)], block_tokens=bt, n_q_heads=32,
+                            n_kv_heads=8, split_kv=True)
+    assert plan.work_flags == _lib.RCB_WORK_SPLIT_ONLY
+    assert plan.n_combine == 8 and plan.n_work > 8 and plan.n_part_slots == plan.n_work
 
 
 # ---------------------------------------------------------------- rope + kv write

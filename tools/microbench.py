@@ -192,6 +192,10 @@ def bench_attn():
         # a decode step: one new token per request over its cached context (HBM-bound)
         ("mistral decode a1056 b1 x64", 32, 8, 64, [(1056, 1)] * 64),
         ("mistral decode a4096 b1 x64", 32, 8, 64, [(4096, 1)] * 64),
+        # one request (the TTFT engine's single-server decode step / cached-prefix prompt):
+        # 8 items, split-KV across the SMs
+        ("mistral decode a1056 b1 x1", 32, 8, 64, [(1056, 1)]),
+        ("mistral hit a1024 b32 x1", 32, 8, 64, [(1024, 32)]),
     ]
     only = os.environ.get("MB_CASE")
     for name, hq, hkv, bt, reqs in cases:

@@ -440,7 +440,10 @@ def run_ours(args, dist: Dist):
                 "gpu_tier_tokens": w.gpu_capacity_tokens,
                 "host_tier_tokens": w.host_capacity_tokens,
                 "parallelism": f"dp{dist.world} (tree replicas) + corpus shards",
-                "l2": "inputs larger than L2 (corpus scan 154 MB, KV pages ~135 MB/request)",
+                "l2": (f"inputs larger than L2 (corpus shard scan "
+                       f"{retr.bytes_per_scan / 1e6:.0f} MB, KV pages "
+                       f"{shape.kv_bytes_per_token * int(w.doc_tokens_mean) * w.k / 1e6:.0f} "
+                       f"MB of cached documents per request)"),
             },
             "kv_geometry": {"source_shape": shape.name, "n_layers": shape.n_layers,
                             "n_q_heads": shape.n_q_heads, "n_kv_heads": shape.n_kv_heads,

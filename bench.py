@@ -393,7 +393,8 @@ def run_ours(args, dist: Dist):
     # device time per retrieval call (scan + PDL-chained merge) without host launch gaps:
     # the step's own call replayed back to back from a CUDA graph (corpus >> L2)
     dev_scan_ms = retr.device_ms()
-    scan_gbs = retr.bytes_per_scan / (dev_scan_ms / 1e3) / 1e9
+    scan_bytes = retr.bytes_per_scan
+    scan_gbs = scan_bytes / (dev_scan_ms / 1e3) / 1e9
     d2h = st1["d2h_bytes"] - st0["d2h_bytes"]
     h2d = st1["h2d_bytes"] - st0["h2d_bytes"]
     copy_ms = c0.elapsed_time(c1)
@@ -441,7 +442,7 @@ def run_ours(args, dist: Dist):
                 "host_tier_tokens": w.host_capacity_tokens,
                 "parallelism": f"dp{dist.world} (tree replicas) + corpus shards",
                 "l2": (f"inputs larger than L2 (corpus shard scan "
-                       f"{retr.bytes_per_scan / 1e6:.0f} MB, KV pages "
+                       f"{scan_bytes / 1e6:.0f} MB, KV pages "
                        f"{shape.kv_bytes_per_token * int(w.doc_tokens_mean) * w.k / 1e6:.0f} "
                        f"MB of cached documents per request)"),
             },

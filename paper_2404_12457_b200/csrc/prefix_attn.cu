@@ -108,6 +108,14 @@ struct Smem {
 //   pair item  (n1 > 0): softmax WG w owns query tile Q_w over steps j < n_w
 //   split item (n1 == 0, a lone query tile): WG w owns the steps j with j % 2 == w of Q0,
 //              each WG keeps its own (m, l, O_w) and the epilogue merges the two
+#ifndef RCB_OTMA
+#define RCB_OTMA 1
+#endif
+// O of a full query tile leaves through a TMA store staged in the finished item's Q
+// buffer (its last QK retired before the last PV, i.e. before O_w was complete); the
+// epilogue's arrival on Q_empty then releases the buffer for Q(ii + 2).  Ragged tiles and
+// split-KV parts keep the per-lane stores.
+constexpr bool kOTma = RCB_OTMA != 0;
 constexpr int kItemInts = 8;
 struct Item {
   int q_start, q_len, q_pos0, blk_begin, blk_count, qp, kvh, n0, n1;
@@ -154,6 +162,7 @@ template <int HD, int G, int BT, bool SPLIT>
 __global__ void __launch_bounds__(kThreads, 1)
     prefix_prefill_kernel(const __grid_constant__ CUtensorMap tm_q,
                           const __grid_constant__ CUtensorMap tm_kv,
+                          const __grid_constant__ CUtensorMap tm_o,
                           __nv_bfloat16* __restrict__ out, int n_q_heads, int layer,
                           const int* __restrict__ blk_ids, const int* __restrict__ blk_valid,
                           const int* __restrict__ blk_pos, const int* __restrict__ work,
@@ -180,7 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bar[kQFull0 + b], 1);
-      mbar_init(&bar[kQEmpty0 + b], 1);
+      mbar_init(&bar[kQEmpty0 + b], kOTma ? 2 : 1);  // MMA (last QK) + epilogue (O store)
       mbar_init(&bar[kQReady0 + b], kRows);
       mbar_init(&bar[kSFull0 + b], 1);
       mbar_init(&bar[kPFull0 + b], kRows);
@@ -669,9 +678,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     int oc[2] = {0, 0};
     // rows of query tile qt = (sum_w c_w O_w) / (sum_w c_w l_w), c_w = 2^(m_w - max m) over
     // the WGs that worked on it (one for a pair item's tile, both for a split item)
-    auto epilogue = [&](const Item& it, int qt, bool use0, bool use1) {
+    auto epilogue = [&](const Item& it, int qt, bool use0, bool use1, int qb) {
       const int tok = (2 * it.qp + qt) * TQ + t_local;
       const bool row_valid = tok < it.q_len;
+      // a full tile (every token valid) is staged in its Q buffer and TMA-stored
+      const bool stage = kOTma && !SPLIT && (2 * it.qp + qt + 1) * TQ <= it.q_len;
+      const uint32_t stg = smem_u32(sQ) + (qb * S::kQT + (SPLIT ? 0 : qt)) * S::kQ;
       float2 ml0 = make_float2(-INFINITY, 0.f), ml1 = ml0;
       if (use0) {
         mbar_wait(&bar[kLFull0 + 0], oc[0] & 1);
@@ -729,6 +741,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                          :: "l"(prow + i), "f"(o[i]), "f"(o[i + 1]), "f"(o[i + 2]), "f"(o[i + 3]),
                             "f"(o[i + 4]), "f"(o[i + 5]), "f"(o[i + 6]), "f"(o[i + 7])
                          : "memory");
+        } else if (stage) {
+          // SW128 Q-tile layout: [half][row][128 B], 16-byte chunk c of row r at (c ^ (r & 7))
+          const uint32_t rb = stg + (ch >> 1) * 16384 + (row >> 3) * 1024 + (row & 7) * 128;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int c16 = (ch & 1) * 4 + k;
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};"
+                         :: "r"(rb + ((c16 ^ (row & 7)) << 4)),
+                            "r"(pack_bf16(o[8 * k + 0], o[8 * k + 1])),
+                            "r"(pack_bf16(o[8 * k + 2], o[8 * k + 3])),
+                            "r"(pack_bf16(o[8 * k + 4], o[8 * k + 5])),
+                            "r"(pack_bf16(o[8 * k + 6], o[8 * k + 7]))
+                         : "memory");
+          }
         } else if (row_valid) {
 #pragma unroll
           for (int i = 0; i < 32; i += 16) {
@@ -740,6 +766,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                             "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
                          : "memory");
           }
+        }
+      }
+      if (stage) {
+        fence_proxy_async_smem();   // generic-proxy smem writes -> visible to the TMA store
+        named_bar_sync(1, kRows);   // the whole tile is staged
+        if (row == 0) {
+          const int t0 = it.q_start + (2 * it.qp + qt) * TQ;
+#pragma unroll
+          for (int h = 0; h < HD / 64; ++h)
+            tma_store_3d(&tm_o, stg + h * 16384, h * 64, it.kvh * G, t0);
+          tma_store_commit();
         }
       }
       if (use0) ++oc[0];
@@ -757,13 +794,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int ii = 0; ii < n_mine; ++ii) {
       const Item it = item_of(ii);
       if (it.split()) {
-        epilogue(it, 0, true, it.has(1));
+        epilogue(it, 0, true, it.has(1), ii & 1);
       } else {
-        epilogue(it, 0, true, false);
-        if (it.has(1)) epilogue(it, 1, false, true);
+        epilogue(it, 0, true, false, ii & 1);
+        if (it.has(1)) epilogue(it, 1, false, true, ii & 1);
+      }
+      if (kOTma && row == 0) {  // the staged O left smem: Q(ii + 2) may land in the buffer
+        tma_store_wait_read();
+        mbar_arrive(&bar[kQEmpty0 + (ii & 1)]);
       }
       if (rope != nullptr && ii + kAhead < n_mine) rotate_q(item_of(ii + kAhead), ii + kAhead);
     }
+    if (kOTma && row == 0) tma_store_wait_all();
     tc_fence_before();
   }
   __syncthreads();
@@ -821,7 +863,7 @@ __global__ void __launch_bounds__(kRows)
 }
 
 template <int HD, int G, int BT, bool SPLIT>
-cudaError_t launch_s(const CUtensorMap& tq, const CUtensorMap& tkv, void* out, int n_q_heads,
+cudaError_t launch_s(const CUtensorMap& tq, const CUtensorMap& tkv, const CUtensorMap& to, void* out, int n_q_heads,
                      int layer, const int* blk_ids, const int* blk_valid,
                      const int* blk_pos, const int* work, int n_work, float scale_log2,
                      const float2* rope, float* part_o, float2* part_ml, cudaStream_t stream) {
@@ -841,45 +883,45 @@ cudaError_t launch_s(const CUtensorMap& tq, const CUtensorMap& tkv, void* out, i
     if (sms <= 0) sms = 148;
   }
   const int grid = n_work < sms ? n_work : sms;
-  kern<<<grid, kThreads, smem, stream>>>(tq, tkv, static_cast<__nv_bfloat16*>(out), n_q_heads,
+  kern<<<grid, kThreads, smem, stream>>>(tq, tkv, to, static_cast<__nv_bfloat16*>(out), n_q_heads,
                                         layer, blk_ids, blk_valid, blk_pos, work, n_work,
                                         scale_log2, rope, part_o, part_ml);
   return cudaGetLastError();
 }
 
 template <int HD, int G, int BT>
-cudaError_t launch_t(bool split, const CUtensorMap& tq, const CUtensorMap& tkv, void* out,
+cudaError_t launch_t(bool split, const CUtensorMap& tq, const CUtensorMap& tkv, const CUtensorMap& to, void* out,
                      int n_q_heads, int layer, const int* bi, const int* bv, const int* bp,
                      const int* work, int n_work, float sl2, const float2* rope,
                      float* po, float2* pm, cudaStream_t st) {
-  return split ? launch_s<HD, G, BT, true>(tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st)
-               : launch_s<HD, G, BT, false>(tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
+  return split ? launch_s<HD, G, BT, true>(tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st)
+               : launch_s<HD, G, BT, false>(tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
 }
 
 template <int HD, int G>
-cudaError_t launch_bt(bool split, int bt, const CUtensorMap& tq, const CUtensorMap& tkv, void* out,
+cudaError_t launch_bt(bool split, int bt, const CUtensorMap& tq, const CUtensorMap& tkv, const CUtensorMap& to, void* out,
                       int n_q_heads, int layer, const int* bi, const int* bv,
                       const int* bp, const int* work, int n_work, float sl2, const float2* rope,
                       float* po, float2* pm, cudaStream_t st) {
   switch (bt) {
-    case 16: return launch_t<HD, G, 16>(split, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
-    case 32: return launch_t<HD, G, 32>(split, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
-    case 64: return launch_t<HD, G, 64>(split, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
-    case 128: return launch_t<HD, G, 128>(split, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
+    case 16: return launch_t<HD, G, 16>(split, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
+    case 32: return launch_t<HD, G, 32>(split, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
+    case 64: return launch_t<HD, G, 64>(split, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
+    case 128: return launch_t<HD, G, 128>(split, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
 template <int HD>
-cudaError_t launch_g(bool split, int g, int bt, const CUtensorMap& tq, const CUtensorMap& tkv, void* out,
+cudaError_t launch_g(bool split, int g, int bt, const CUtensorMap& tq, const CUtensorMap& tkv, const CUtensorMap& to, void* out,
                      int n_q_heads, int layer, const int* bi, const int* bv,
                      const int* bp, const int* work, int n_work, float sl2, const float2* rope,
                      float* po, float2* pm, cudaStream_t st) {
   switch (g) {
-    case 1: return launch_bt<HD, 1>(split, bt, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
-    case 2: return launch_bt<HD, 2>(split, bt, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
-    case 4: return launch_bt<HD, 4>(split, bt, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
-    case 8: return launch_bt<HD, 8>(split, bt, tq, tkv, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
+    case 1: return launch_bt<HD, 1>(split, bt, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
+    case 2: return launch_bt<HD, 2>(split, bt, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
+    case 4: return launch_bt<HD, 4>(split, bt, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
+    case 8: return launch_bt<HD, 8>(split, bt, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -908,7 +950,15 @@ int prefix_prefill(const void* q, int64_t q_row_stride, void* o, int total_q_tok
   if (n_kv_heads <= 0 || n_q_heads % n_kv_heads != 0) return set_error(RCB_ERR_ARG, "bad head counts");
   const int g = n_q_heads / n_kv_heads;
   if (layer < 0 || layer >= n_layers) return set_error(RCB_ERR_ARG, "layer out of range");
-  CUtensorMap tq, tkv;
+  CUtensorMap tq, tkv, to;
+  {
+    // output O [T][Hq][HD] (contiguous): the same box as a Q tile, for the TMA store
+    const uint64_t dims[3] = {(uint64_t)head_dim, (uint64_t)n_q_heads, (uint64_t)total_q_tokens};
+    const uint64_t strides[2] = {(uint64_t)head_dim * 2, (uint64_t)n_q_heads * head_dim * 2};
+    const uint32_t box[3] = {64, (uint32_t)g, (uint32_t)(128 / g)};
+    int rc = encode_tma_bf16(&to, o, 3, dims, strides, box);
+    if (rc != RCB_OK) return rc;
+  }
   {
     const uint64_t dims[3] = {(uint64_t)head_dim, (uint64_t)n_q_heads, (uint64_t)total_q_tokens};
     if (q_row_stride < (int64_t)n_q_heads * head_dim || q_row_stride % 8 != 0)
@@ -932,10 +982,10 @@ int prefix_prefill(const void* q, int64_t q_row_stride, void* o, int total_q_tok
   const float sl2 = softmax_scale * 1.4426950408889634f;
   cudaError_t e =
       head_dim == 128
-          ? attn::launch_g<128>(split_only, g, block_tokens, tq, tkv, o, n_q_heads, layer, blk_ids,
+          ? attn::launch_g<128>(split_only, g, block_tokens, tq, tkv, to, o, n_q_heads, layer, blk_ids,
                                 blk_valid, blk_pos, work, n_work, sl2,
                                 static_cast<const float2*>(rope_table), part_o, part_ml, stream)
-          : attn::launch_g<64>(split_only, g, block_tokens, tq, tkv, o, n_q_heads, layer, blk_ids,
+          : attn::launch_g<64>(split_only, g, block_tokens, tq, tkv, to, o, n_q_heads, layer, blk_ids,
                                blk_valid, blk_pos, work, n_work, sl2,
                                static_cast<const float2*>(rope_table), part_o, part_ml, stream);
   if (e != cudaSuccess) return set_cuda_error(e, "prefix_prefill launch");

@@ -609,9 +609,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // Work unit = (query tile, token, chunk pair (i, i+HD/2) of 8 elements): one 64 B
       // cos/sin slice serves the G rows (heads) of that token.  Consecutive threads take
       // consecutive chunk pairs, so a warp's table reads are contiguous 512 B runs and its
-      // shared accesses hit distinct 16 B chunks of each 128 B swizzled row.  The next
-      // unit's slice is in flight while this one rotates; loops stay rolled (this code
-      // shares the instruction cache with the softmax).
+      // shared accesses hit distinct 16 B chunks of each 128 B swizzled row.  Loops stay
+      // rolled (this code shares the instruction cache with the softmax).
       constexpr int CP = HD / 16;  // chunk pairs per row
       constexpr int U = TQ * CP;   // units per query tile
       const int qb = ii & 1;
@@ -622,16 +621,38 @@ __global__ void __launch_bounds__(kThreads, 1)
         return reinterpret_cast<const float4*>(rope + static_cast<int64_t>(it.q_pos0 + tok) *
                                                           (HD / 2) + cp * 8);
       };
-      float4 cur[4], nxt[4];
+      // Small G (MHA-like: 8-16 units per thread per item): a thread's units share its
+      // chunk pair and step 128 / CP tokens = D positions at a time (within and across
+      // the two tiles), so (cos, sin) of unit k+1 follow from unit k by the angle-addition
+      // rotation by D * theta: one table slice per call instead of one L2 round trip per
+      // unit, which made the G = 1 rotation latency-bound (LLaMA2 miss batch 148 -> 115 us).
+      // (cos, sin)(D * theta) = table row 1 doubled log2(D) times.  G >= 4 (2-4 units per
+      // thread) keeps the per-unit slices with one prefetched ahead: measured faster there.
+      constexpr int D = 128 / CP;
+      constexpr bool kStep = G <= 2;
+      float4 cur[4], nxt[4], stp[4];
       if (row < total) {
         const float4* t = slice(row);
 #pragma unroll
         for (int e = 0; e < 4; ++e) cur[e] = __ldg(t + e);
+        if constexpr (kStep) {
+          const float4* t1 = reinterpret_cast<const float4*>(rope + (HD / 2) + (row % CP) * 8);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) stp[e] = __ldg(t1 + e);
+#pragma unroll
+          for (int d = 1; d < D; d *= 2)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {  // double the angle: (c, s) -> (c^2 - s^2, 2 s c)
+              const float4 a = stp[e];
+              stp[e] = make_float4(a.x * a.x - a.y * a.y, 2.f * a.y * a.x,
+                                   a.z * a.z - a.w * a.w, 2.f * a.w * a.z);
+            }
+        }
       }
       mbar_wait(&bar[kQFull0 + qb], (ii >> 1) & 1);
 #pragma unroll 1
       for (int u = row; u < total; u += 128) {
-        if (u + 128 < total) {
+        if (!kStep && u + 128 < total) {
           const float4* t = slice(u + 128);
 #pragma unroll
           for (int e = 0; e < 4; ++e) nxt[e] = __ldg(t + e);
@@ -670,7 +691,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                        "r"(v1[1]), "r"(v1[2]), "r"(v1[3]));
         }
 #pragma unroll
-        for (int e = 0; e < 4; ++e) cur[e] = nxt[e];
+        for (int e = 0; e < 4; ++e) {
+          if constexpr (kStep) {  // advance D positions: angle + D * theta
+            const float4 a = cur[e], b = stp[e];
+            cur[e] = make_float4(a.x * b.x - a.y * b.y, a.y * b.x + a.x * b.y,
+                                 a.z * b.z - a.w * b.w, a.w * b.z + a.z * b.w);
+          } else {
+            cur[e] = nxt[e];
+          }
+        }
       }
       fence_proxy_async_smem();  // generic-proxy writes -> tensor-core reads
       mbar_arrive(&bar[kQReady0 + qb]);

@@ -234,8 +234,8 @@ def prefix_prefill(q: torch.Tensor, out: torch.Tensor, plan: AttnPlan, pool_base
     if n_q_heads is None:
         n_q_heads = out.shape[1]
     row_stride = q.stride(0)
-    if rope is not None and (rope.dtype != torch.float32 or rope.shape[0] < plan.max_pos
-                             or rope.shape[1] * 2 != head_dim):
+    if rope is not None and (rope.dtype != torch.float32 or rope.shape[0] < max(plan.max_pos, 2)
+                             or rope.shape[1] * 2 != head_dim):  # row 1 seeds the angle steps
         raise ValueError(f"rope table {tuple(rope.shape)} does not cover positions < "
                          f"{plan.max_pos} at head_dim {head_dim}")
     if softmax_scale is None:

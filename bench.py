@@ -117,7 +117,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(loaded), "source": "nvml, 5 ms"}
 
 
-NCU_TAG = "r1f"  # profiles/<tag>_ncu_summary.json: captures of the current kernels
+NCU_TAG = "r1g"  # profiles/<tag>_ncu_summary.json: captures of the current kernels
 
 
 def ncu_traffic(capture: str):

@@ -14,6 +14,9 @@ ncu --set full --clock-control none --import-source on -k regex:prefix_prefill -
 # (the mixed-step case only: 2 plain launches, then the fused-RoPE one is captured)
 MB_CASE="mixed step" ncu --set full --clock-control none --import-source on -k regex:prefix_prefill -s 2 -c 1 \
     -o gpurun_out/${TAG}_attn_mixed python tools/microbench.py attn --ncu > /dev/null 2>&1
+# MHA (G = 1, LLaMA2 shape) with fused RoPE: the third launch of the case is the RoPE one
+MB_CASE="llama2 miss" ncu --set full --clock-control none --import-source on -k regex:prefix_prefill -s 2 -c 1 \
+    -o gpurun_out/${TAG}_attn_mha python tools/microbench.py attn --ncu > /dev/null 2>&1
 # split-only variant (decode step over a 4096-token context: HBM-bound)
 MB_CASE="decode a4096" ncu --set full --clock-control none --import-source on -k regex:prefix_prefill -s 2 -c 1 \
     -o gpurun_out/${TAG}_attn_decode python tools/microbench.py attn --ncu > /dev/null 2>&1

@@ -9,7 +9,7 @@
   is the top-k over the union of every shard's first (s+1)/S rows.
 
 ``Dist`` wraps torch.distributed (NCCL on the GPU box, gloo in CPU tests);
-collectives use list-based all_gather so both backends work.
+all_gather writes one [world, ...] buffer (all_gather_into_tensor, NCCL and gloo).
 """
 
 from __future__ import annotations
@@ -34,8 +34,10 @@ class Dist:
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
         self.device = "cpu"
+        self.backend = None
 
     def init(self, backend: str = "nccl") -> "Dist":
+        self.backend = backend
         self.device = "cuda" if backend == "nccl" else "cpu"
         if self.world > 1:
             import torch.distributed as dist
@@ -67,9 +69,13 @@ class Dist:
         """[world, *t.shape] (rank order)."""
         if self.pg is None:
             return t.unsqueeze(0)
-        parts = [torch.empty_like(t) for _ in range(self.world)]
-        self.pg.all_gather(parts, t.contiguous())
-        return torch.stack(parts)
+        if self.backend == "gloo" and t.is_cuda:  # gloo: list form for device tensors
+            parts = [torch.empty_like(t) for _ in range(self.world)]
+            self.pg.all_gather(parts, t.contiguous())
+            return torch.stack(parts)
+        out = torch.empty(self.world * t.numel(), dtype=t.dtype, device=t.device)
+        self.pg.all_gather_into_tensor(out, t.contiguous().reshape(-1))  # one buffer, no stack
+        return out.view((self.world,) + tuple(t.shape))
 
     def close(self) -> None:
         if self.pg is not None:

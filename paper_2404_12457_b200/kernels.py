@@ -275,6 +275,9 @@ def silu_mul(gate_up: torch.Tensor, stream=None) -> torch.Tensor:
     return out
 
 
+MAX_SCAN_QUERIES = 64  # queries per rcb_retrieval_topk call (rcb_retrieval.cu check_args)
+
+
 class RetrievalWorkspace:
     def __init__(self, n_rows: int, n_queries: int, k: int, n_stages: int, device="cuda"):
         self.nbytes = int(load().rcb_retrieval_workspace_bytes(n_rows, n_queries, k, n_stages))

@@ -113,6 +113,102 @@ def test_two_rank_gloo_shards_and_replicas():
     assert got == {0: "ok", 1: "ok"}, got
 
 
+def _oracle_scan(corpus_np):
+    from oracle import topk_oracle
+
+    def scan(corpus, q, k, S, off):
+        ids, sc = topk_oracle.staged_topk(corpus_np, q.float().numpy().astype(np.float64), k, S,
+                                          id_offset=off)
+        return torch.from_numpy(ids), torch.from_numpy(sc.astype(np.float32))
+
+    return scan
+
+
+def _oracle_merge(gi, gs):
+    k = gi.shape[-1]
+    return torch.from_numpy(_merge(gi.numpy(), gs.numpy(), k)), None
+
+
+def _provider_worker(rank, port, results):
+    """The package's sharded StageProvider (ShardedRetriever: query all-gather, per-shard
+    scan, list all-gather, merge) driving a DSP desk run on each rank's routed sub-trace.
+    The scan and merge are the oracle's here (no GPU); the collectives, padding,
+    lockstep rounds and routing are the product's."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(WORLD), LOCAL_RANK=str(rank))
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    from ragsim.config import RunConfig
+    from ragsim.speculation import StagedRetrieval
+
+    from oracle import topk_oracle
+    from paper_2404_12457_b200 import cache, synth
+    from paper_2404_12457_b200.dist import Dist, route, shard_bounds
+    from paper_2404_12457_b200.pool import accounting_pool
+    from paper_2404_12457_b200.retrieval import GpuStageProvider, ShardedRetriever, synthetic_query_fn
+    from tests.golden.make_golden import DESK, desk_trace
+
+    d = Dist().init("gloo")
+    try:
+        n_docs = 1500
+        trace, sizes = desk_trace(seed=0, duration_s=200.0, rate=0.3, pool=300)
+        sub = route(trace, rank, WORLD)
+        cfg = RunConfig(host_capacity_tokens=32768, stage_count=4, stage_interval_ms=50.0,
+                        convergence_stage=2, prefill_chunk_ms=25.0, dsp=True, seed=0,
+                        validate=True, **DESK)
+        lo, hi = shard_bounds(n_docs, rank, WORLD)
+        shard = synth.corpus_int(hi - lo, seed=0, row_offset=lo)
+        qfn = synthetic_query_fn(seed=0, kind="int")
+        retr = ShardedRetriever(torch.from_numpy(shard.astype(np.float32)), lo, cfg.k,
+                                cfg.stage_count, d, batch=8, scan=_oracle_scan(shard),
+                                merge=_oracle_merge)
+        sp = GpuStageProvider(retr.corpus, qfn, k=cfg.k, n_stages=cfg.stage_count,
+                              stage_interval_ms=cfg.stage_interval_ms, trace=sub, retriever=retr)
+        bounds = [shard_bounds(n_docs, r, WORLD) for r in range(WORLD)]
+        shards = [synth.corpus_int(b - a, seed=0, row_offset=a) for a, b in bounds]
+        full = np.concatenate(shards)
+
+        def oracle_provider(req):
+            q = qfn(req)[None]
+            ids, _ = topk_oracle.sharded_staged_topk(shards, [a for a, _ in bounds], q, cfg.k,
+                                                     cfg.stage_count)
+            one, _ = topk_oracle.staged_topk(full, q, cfg.k, cfg.stage_count)
+            assert np.array_equal(ids[0, -1], one[0, -1])  # final stage = 1 shard
+            return StagedRetrieval(tuple(tuple(int(x) for x in st) for st in ids[0]),
+                                   cfg.stage_interval_ms)
+
+        r_sh, _ = cache.run_tiered(cfg, sub, sizes, pool=accounting_pool(4096, 8192, 16),
+                                   stage_provider=sp)
+        r_or, _ = cache.run_tiered(cfg, sub, sizes, pool=accounting_pool(4096, 8192, 16),
+                                   stage_provider=oracle_provider)
+        assert r_sh.to_json(cfg) == r_or.to_json(cfg)
+        assert r_sh.aggregates()["speculations"] > 0
+        d.barrier()
+        results.put((rank, "ok"))
+    except Exception as exc:  # pragma: no cover - surfaced by the parent
+        import traceback
+
+        results.put((rank, traceback.format_exc()[-1500:]))
+    finally:
+        d.close()
+
+
+@pytest.mark.skipif(not ragsim_available(), reason="ragsim not importable")
+def test_two_rank_sharded_stage_provider_dsp_run():
+    ctx = mp.get_context("spawn")
+    results = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_provider_worker, args=(r, port, results)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    got = dict(results.get(timeout=300) for _ in range(WORLD))
+    for p in procs:
+        p.join(timeout=60)
+    assert got == {0: "ok", 1: "ok"}, got
+
+
 def test_shard_bounds_and_route_partition():
     from paper_2404_12457_b200.dist import route, shard_bounds
 

@@ -36,7 +36,7 @@ def test_engine_with_gpu_stages_matches_oracle_stages():
                     convergence_stage=2, prefill_chunk_ms=25.0, dsp=True, seed=0, validate=True,
                     **DESK)
     corpus = synth.corpus_int(n_docs, seed=0)
-    qfn = synthetic_query_fn(seed=0)
+    qfn = synthetic_query_fn(seed=0, kind="int")  # exact scores: byte-identical reports
     gpu = GpuStageProvider(torch.from_numpy(corpus.astype(np.float32)).cuda().to(torch.bfloat16),
                            qfn, k=cfg.k, n_stages=cfg.stage_count,
                            stage_interval_ms=cfg.stage_interval_ms, trace=trace)

@@ -125,7 +125,7 @@ def test_retrieval_reproduces_ground_truth_docs():
     corpus = synth.corpus_int(n_rows, seed=11)
     rng = np.random.default_rng(5)
     seqs = [tuple(int(x) for x in rng.choice(n_rows, size=k, replace=False)) for _ in range(48)]
-    q = synth.build_queries(lambda ids: corpus[ids], seqs)
+    q = synth.build_queries_int(lambda ids: corpus[ids], seqs)
     c_dev = torch.from_numpy(corpus.astype(np.float32)).to("cuda", torch.bfloat16)
     q_dev = torch.from_numpy(q.astype(np.float32)).to("cuda", torch.bfloat16)
     ids, _ = kernels.retrieval_topk(c_dev, q_dev, k, 4)

@@ -32,3 +32,18 @@ def test_two_rank_bench_on_one_gpu():
     assert d["n_gpus"] == 2 and d["value"] > 0
     assert d["retrieval_final_stage_matches_ground_truth"]
     assert d["e2e"]["retrieval_matches_ground_truth"]
+
+
+def test_two_rank_sharded_stage_provider_on_one_gpu():
+    """GpuStageProvider(comm=...) with the real kernels: per-rank corpus shards, lockstep
+    query all-gather, shard scans, list all-gather and device merge under a DSP run."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29543",
+           os.path.join("tests", "sharded_provider_run.py")]
+    res = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    rows = [json.loads(l) for l in res.stdout.splitlines() if l.startswith("{")]
+    assert sorted(r["rank"] for r in rows) == [0, 1]
+    for r in rows:
+        assert r["identical"] and r["finals_equal_unsharded"], r
+        assert r["speculations"] > 0 and r["requests"] > 0

@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--single-device", action="store_true")
     ap.add_argument("--gpu-tier-tokens", type=int, default=0)
+    ap.add_argument("--ref-sample", type=int, default=1,
+                    help="requests per step timed through the reference CPU path")
     return ap.parse_args()
 
 
@@ -176,21 +178,20 @@ def run_ours(args, dist: Dist):
     from paper_2404_12457_b200.pool import accounting_pool
     from paper_2404_12457_b200.retrieval import ShardedRetriever
     from paper_2404_12457_b200.workloads import pool_blocks
-    from ragsim.cost_model import synthetic_profile
 
     torch.cuda.set_device(0 if args.single_device else dist.local)
     dist.init(args.backend)
     dist.device = "cuda"
     w, R, steps, sizes, (lo, hi) = build_workload(args, dist)
+    raw_steps = list(steps)  # the planning loop below keeps only each step's admitted prefix
     if args.gpu_tier_tokens:
         import dataclasses as _dc
 
         w = _dc.replace(w, gpu_capacity_tokens=args.gpu_tier_tokens)
     shape = w.model
-    min_doc = min(sizes.values())
-    ng = pool_blocks(w.gpu_capacity_tokens, w.block_tokens, min_doc, R * (w.k + 1))
-    nh = pool_blocks(w.host_capacity_tokens, w.block_tokens, min_doc, 0)
-    profile = synthetic_profile()
+    ng = pool_blocks(w.gpu_capacity_tokens, w.block_tokens, sizes.values(), R * (w.k + 1))
+    nh = pool_blocks(w.host_capacity_tokens, w.block_tokens, sizes.values(), 0)
+    profile, profile_src = tree_profile(w)
     copy_stream = torch.cuda.Stream()
     compute = torch.cuda.current_stream()
 
@@ -352,7 +353,8 @@ def run_ours(args, dist: Dist):
 
     result = None
     if dist.rank == 0:
-        cpu = None if args.no_cpu_baseline or dist.world > 1 else cpu_baseline(w, plans[W:W + K], R)
+        cpu = None if args.no_cpu_baseline or dist.world > 1 else \
+            cpu_baseline(args, w, R, raw_steps, sizes, profile, profile_src)
         result = {
             "metric": METRIC,
             "value": round(value, 3),
@@ -368,22 +370,8 @@ def run_ours(args, dist: Dist):
             "data": "synthetic (ragsim generators: Zipf 0.97 docs x 512 tok; unit-norm "
                     "Irwin-Hall 768-d bf16 embeddings, queries built from the ground-truth "
                     "docs; random bf16 activations in place of model projections)",
-            "config": {
-                "workload": w.name,
-                "batch_per_gpu": R,
-                "corpus_docs": w.num_docs,
-                "doc_tokens": int(w.doc_tokens_mean),
-                "k": w.k,
-                "stages": w.n_stages,
-                "block_tokens": w.block_tokens,
-                "gpu_tier_tokens": w.gpu_capacity_tokens,
-                "host_tier_tokens": w.host_capacity_tokens,
-                "parallelism": f"dp{dist.world} (tree replicas) + corpus shards",
-                "l2": (f"inputs larger than L2 (corpus shard scan "
-                       f"{scan_bytes / 1e6:.0f} MB, KV pages "
-                       f"{shape.kv_bytes_per_token * int(w.doc_tokens_mean) * w.k / 1e6:.0f} "
-                       f"MB of cached documents per request)"),
-            },
+            "config": bench_config(w, R, dist.world),
+            "tree_profile": profile_src,
             "kv_geometry": {"source_shape": shape.name, "n_layers": shape.n_layers,
                             "n_q_heads": shape.n_q_heads, "n_kv_heads": shape.n_kv_heads,
                             "head_dim": shape.head_dim,
@@ -586,13 +574,17 @@ def run_e2e(args, dist, w, R, steps, planner, device, dpool, retr, qkv, q_rot, o
     # software pipeline: step i+1's retrieval runs on its own stream while step i's
     # prefill runs, so the host's admissions/commits overlap device work
     launch_retrieval(0)
+    carry = []  # (request, retrieved docs) deferred by a full GPU tier: served first next step
     for i, batch in enumerate(extra):
         ids_ready[i & 1].synchronize()
         if i + 1 < len(extra):
             launch_retrieval(i + 1)
-        docs = [tuple(int(x) for x in row) for row in ids_host[i & 1][:, -1].numpy()]
+        docs = [tuple(int(x) for x in row) for row in ids_host[i & 1][: len(batch), -1].numpy()]
         ok &= docs == [r.doc_sequence for r in batch]
-        adm = planner.admit_batch([(r.id, d, r.prompt_tokens) for r, d in zip(batch, docs)])
+        todo = carry + list(zip(batch, docs))
+        cand = todo[:R]
+        adm = planner.admit_batch([(r.id, d, r.prompt_tokens) for r, d in cand])
+        carry = todo[len(adm):]
         served += len(adm)
         plan = StepPlan(adm, [], [])
         device.prepare_device(plan)
@@ -613,7 +605,7 @@ def run_e2e(args, dist, w, R, steps, planner, device, dpool, retr, qkv, q_rot, o
     el = time.perf_counter() - t0
     el = dist.max(el)
     served = dist.sum(float(served))
-    return {"value": round(served / el, 3), "unit": "req/s",
+    return {"value": round(served / el, 3), "unit": "req/s", "deferred_at_end": len(carry),
             "doc_hit_rate": round(hits / max(1, docs_total), 4),
             "h2d_bytes_per_step": int(h2d // K), "d2h_bytes_per_step": int(d2h // K),
             "ms_per_step": round(el * 1e3 / K, 3), "retrieval_matches_ground_truth": bool(ok),
@@ -623,111 +615,88 @@ def run_e2e(args, dist, w, R, steps, planner, device, dpool, retr, qkv, q_rot, o
 
 
 # ---------------------------------------------------------------------- CPU baselines
-def cpu_step_sample(w, plan, n_req: int, n_layers: int, corpus_cpu, queries_cpu):
-    """The oracle CPU path on a bounded sample: exact top-k over the corpus for
-    n_req queries, then per layer KV gather + fp32 prefix attention."""
-    from oracle import attn_oracle, topk_oracle
+def tree_profile(w):
+    """PGDSF's cost profile for the bench tree (tree.py:240): the B200-measured T(alpha, beta)
+    grid of this model shape (profiles/<shape>_b200_profile.csv, written by profile.py via
+    tools/ttft_curve.py), else ragsim's synthetic profile.  Both arms use the same one."""
+    from ragsim.cost_model import load_profile_csv, synthetic_profile
 
-    shape = w.model
-    adms = plan.admissions[:n_req]
-    t0 = time.perf_counter()
-    topk_oracle.staged_topk(corpus_cpu, queries_cpu[:n_req], w.k, w.n_stages)
-    t_ret = time.perf_counter() - t0
-    inputs = []
-    for a in adms:
-        # the request's KV pages in a host pool, gathered per layer by the oracle
-        pool = torch.randn((len(a.blocks), 1, 2, shape.n_kv_heads, w.block_tokens, shape.head_dim),
-                           dtype=torch.bfloat16)
-        q = torch.randn((a.beta, shape.n_q_heads, shape.head_dim))
-        inputs.append((q, pool, [(a.beta, a.alpha, list(range(len(a.blocks))), a.valid)]))
-    t0 = time.perf_counter()
-    for q, pool, reqs in inputs:
-        for _ in range(n_layers):
-            attn_oracle.prefix_prefill(q, pool, reqs, 0)
-    t_attn = time.perf_counter() - t0
-    return t_ret, t_attn
+    path = os.path.join(ROOT, "profiles", f"{w.shape}_b200_profile.csv")
+    if os.path.exists(path):
+        return load_profile_csv(path), os.path.relpath(path, ROOT)
+    return synthetic_profile(), "ragsim synthetic_profile (no B200 grid committed for this shape)"
 
 
-def cpu_baseline(w, plans, R, budget_s: float = 15.0):
-    from paper_2404_12457_b200 import synth
+def bench_config(w, R: int, world: int) -> dict:
+    """The `config` object of both arms (identical by construction)."""
+    shard_rows = -(-w.num_docs // world)
+    return {
+        "workload": w.name,
+        "batch_per_gpu": R,
+        "corpus_docs": w.num_docs,
+        "doc_tokens": int(w.doc_tokens_mean),
+        "k": w.k,
+        "stages": w.n_stages,
+        "block_tokens": w.block_tokens,
+        "gpu_tier_tokens": w.gpu_capacity_tokens,
+        "host_tier_tokens": w.host_capacity_tokens,
+        "parallelism": f"dp{world} (tree replicas) + corpus shards",
+        "l2": (f"inputs larger than L2 (corpus shard scan {shard_rows * 768 * 2 / 1e6:.0f} MB, "
+               f"KV pages {w.model.kv_bytes_per_token * int(w.doc_tokens_mean) * w.k / 1e6:.0f} "
+               f"MB of cached documents per request)"),
+    }
 
-    threads = len(os.sched_getaffinity(0))
-    torch.set_num_threads(threads)
-    plan = plans[0]
-    n_req = min(4, len(plan.admissions))
-    corpus_cpu = synth.corpus_int(w.num_docs, seed=w.seed)
-    q = synth.build_queries(lambda ids: corpus_cpu[ids], [a.docs for a in plan.admissions])
-    t_ret, t_attn = cpu_step_sample(w, plan, n_req, 1, corpus_cpu, q)
-    # per request: retrieval share + all layers of attention
-    per_req = t_ret / n_req + t_attn / n_req * w.model.n_layers
-    return {"value": round(1.0 / per_req, 4), "unit": "req/s", "cores": threads, "kind": "port",
-            "sample": f"{n_req} requests of one step: numpy exact staged top-k over "
-                      f"{w.num_docs} docs + 1 of {w.model.n_layers} layers of fp32 CPU "
-                      f"prefix attention (torch, {threads} threads), extrapolated to all layers"}
+
+def cpu_baseline(args, w, R, steps, sizes, profile, profile_src) -> dict:
+    """The reference CPU path (oracle/ref_path.py) on a bounded sample: 2 timed steps of 2
+    requests each, plus ragsim's host decision time per request (1 core) and a CPU
+    KV-gather GB/s comparator."""
+    from oracle import ref_path
+
+    res = ref_path.run_cpu_path(w, steps, sizes, profile, R=R, n_warm=args.cache_warm_steps,
+                                n_steps=2, n_sample=2)
+    block_bytes = w.block_tokens * w.model.kv_bytes_per_token
+    return {"value": round(res["value"], 4), "unit": "req/s", "cores": res["cores"],
+            "kind": "port", "sample": res["sample"] + f"; {res['steps']} timed steps",
+            "doc_hit_rate": res["doc_hit_rate"],
+            "host_decision": ref_path.host_decision_us(
+                w, os.path.join(ROOT, profile_src) if profile_src.endswith(".csv") else None),
+            "kv_gather": ref_path.cpu_gather_gbs(block_bytes, n_blocks=max(32, int(2e9 // block_bytes)),
+                                                 n_pick=min(32, max(4, int(1e9 // block_bytes))))}
 
 
 def run_reference(args, dist: Dist):
-    """--impl reference: the reference's CPU path (ragsim decisions + the oracle
-    port of the kernels) on the host cores, bounded sample per step."""
+    """--impl reference: the reference's CPU path on the host cores (oracle/ref_path.py):
+    ragsim's unmodified KnowledgeTree decisions + the oracle port of the three kernels,
+    each step a bounded sample of the GPU arm's step, every timed second measured.
+    Under torchrun only rank 0 runs."""
     if dist.world > 1 and dist.rank != 0:
         return
-    from paper_2404_12457_b200 import synth
-    from paper_2404_12457_b200.hotpath import EventLog, HotPath
-    from paper_2404_12457_b200.pool import accounting_pool
-    from paper_2404_12457_b200.workloads import pool_blocks
-    from ragsim.cost_model import synthetic_profile
+    from oracle import ref_path
 
     one = Dist()
     w, R, steps, sizes, _ = build_workload(args, one)
-    threads = len(os.sched_getaffinity(0))
-    torch.set_num_threads(threads)
-    ng = pool_blocks(w.gpu_capacity_tokens, w.block_tokens, min(sizes.values()), R * (w.k + 1))
-    nh = pool_blocks(w.host_capacity_tokens, w.block_tokens, min(sizes.values()), 0)
-    hp = HotPath(w.model, gpu_capacity_tokens=w.gpu_capacity_tokens,
-                 host_capacity_tokens=w.host_capacity_tokens, block_tokens=w.block_tokens,
-                 num_gpu_blocks=ng, num_host_blocks=nh, sizes=sizes, profile=synthetic_profile(),
-                 pool=EventLog(accounting_pool(ng, nh, w.block_tokens)),
-                 indexed_leaves=False)  # the reference's own linear victim scan
-    corpus_cpu = synth.corpus_int(w.num_docs, seed=w.seed)
-    n_req, n_layers_sample = 4, 2
-    times = []
-    n_warm = args.cache_warm_steps
-    from paper_2404_12457_b200.hotpath import StepPlan
-
-    for i, batch in enumerate(steps):
-        t0 = time.perf_counter()
-        adm = hp.admit_batch([(r.id, r.doc_sequence, r.prompt_tokens) for r in batch])
-        t_dec = time.perf_counter() - t0
-        plan = StepPlan(adm, hp.pool.take(), [])
-        if i >= n_warm:
-            q = synth.build_queries(lambda ids: corpus_cpu[ids], [a.docs for a in adm])
-            t_ret, t_attn = cpu_step_sample(w, plan, n_req, n_layers_sample, corpus_cpu, q)
-            per_req = (t_dec / len(adm) + t_ret / n_req
-                       + t_attn / n_req / n_layers_sample * w.model.n_layers)
-            times.append(per_req)
-        t0 = time.perf_counter()
-        for a in adm:
-            hp.commit(a)
-        hp.pool.take()
-        if i >= n_warm and len(times) >= args.warmup + args.steps:
-            break
-    timed = times[args.warmup:] or times
-    per_req = sum(timed) / len(timed)
-    value = 1.0 / per_req
-    sample = (f"per step: ragsim decisions for {R} requests (the reference tree, linear victim "
-              f"scan) + {n_req} requests of numpy exact staged top-k over {w.num_docs} docs + "
-              f"fp32 CPU prefix attention for {n_layers_sample} of {w.model.n_layers} layers, "
-              f"extrapolated per request")
+    profile, profile_src = tree_profile(w)
+    W, K = args.warmup, args.steps
+    res = ref_path.run_cpu_path(w, steps, sizes, profile, R=R, n_warm=args.cache_warm_steps + W,
+                                n_steps=K, n_sample=args.ref_sample)
+    value = res["value"]
+    cpu = {"value": round(value, 4), "unit": "req/s", "cores": res["cores"], "kind": "port",
+           "sample": res["sample"]}
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "req/s",
-        "n_gpus": dist.world, "steps": len(timed), "warmup": args.warmup,
-        "ms_per_step": round(per_req * R * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "n_gpus": dist.world, "steps": res["steps"], "warmup": W,
+        "ms_per_step": round(res["ms_per_step"], 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": w.name, "batch_per_gpu": R},
-        "cpu_baseline": {"value": round(value, 4), "unit": "req/s", "cores": threads,
-                         "kind": "port", "sample": sample},
+        "config": bench_config(w, R, dist.world),
+        "doc_hit_rate": res["doc_hit_rate"],
+        "retrieval_final_stage_matches_ground_truth": res["retrieval_matches_ground_truth"],
+        "tree_profile": profile_src,
+        "cpu_baseline": cpu,
         "e2e": {"value": round(value, 4), "unit": "req/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "warmup_note": (f"{args.cache_warm_steps} cache-warm + {W} warmup steps replayed "
+                        f"untimed on the tree (decisions only)"),
     }))
 
 

@@ -44,9 +44,8 @@ def ttft_curve(w: Workload, profile, *, gpu_tiers, host_tier: int, n_requests: i
                                if stage_interval_ms is not None else {}),
                             **({"decode_ms_per_token": decode_ms_per_token}
                                if decode_ms_per_token is not None else {}))
-            min_doc = min(sizes.values())
-            pool = accounting_pool(pool_blocks(cap, w.block_tokens, min_doc, 8 * (w.k + 1)),
-                                   pool_blocks(host_tier, w.block_tokens, min_doc, 0) or 1,
+            pool = accounting_pool(pool_blocks(cap, w.block_tokens, sizes.values(), 8 * (w.k + 1)),
+                                   pool_blocks(host_tier, w.block_tokens, sizes.values(), 0) or 1,
                                    w.block_tokens)
             sp = stage_provider_fn(trace, cfg) if stage_provider_fn else None
             report, _ = cache.run_tiered(cfg, trace, sizes, pool=pool, stage_provider=sp)

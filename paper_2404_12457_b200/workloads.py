@@ -126,11 +126,15 @@ def make_stream(w: Workload, n_requests: int, rate: float = 1.0, seed: int | Non
     return trace[:n_requests], corpus.size_map()
 
 
-def pool_blocks(capacity_tokens: int, block_tokens: int, min_doc_tokens: int,
+def pool_blocks(capacity_tokens: int, block_tokens: int, doc_sizes,
                 inflight_segments: int) -> int:
-    """Blocks covering a token capacity: ceil(cap/B) + one tail block per
-    resident node + in-flight generation segments."""
+    """Blocks covering a token capacity: ceil(cap/B) + one tail block per resident node
+    whenever any document (node) size is not a multiple of B (at most
+    cap // smallest-doc nodes fit) + in-flight generation segments (+8 slack).
+    ``doc_sizes``: the corpus sizes (iterable or dict values)."""
     if capacity_tokens <= 0:
         return 0
-    tails = 0 if min_doc_tokens % block_tokens == 0 else capacity_tokens // max(1, min_doc_tokens)
+    sizes = list(doc_sizes)
+    ragged = any(int(s) % block_tokens for s in sizes)
+    tails = capacity_tokens // max(1, min(sizes)) if ragged else 0
     return -(-capacity_tokens // block_tokens) + tails + inflight_segments + 8

@@ -17,11 +17,10 @@ import torch  # noqa: E402
 
 
 def main():
+    from oracle import topk_oracle
+    from paper_2404_12457_b200 import cache, synth  # puts ragsim (baseline/_ref) on the path
     from ragsim.config import RunConfig
     from ragsim.speculation import StagedRetrieval
-
-    from oracle import topk_oracle
-    from paper_2404_12457_b200 import cache, synth
     from paper_2404_12457_b200.dist import Dist, route, shard_bounds
     from paper_2404_12457_b200.pool import accounting_pool
     from paper_2404_12457_b200.retrieval import GpuStageProvider, synthetic_query_fn

@@ -145,15 +145,14 @@ def engine(name: str, n_req: int, rate: float):
     pcie = measure_pcie()
     stage_ms = measure_stage_ms(w)
     trace, sizes = make_stream(w, n_req, rate=rate)
-    min_doc = min(sizes.values())
     host = int(os.environ.get("HOST_TIER_TOKENS", 64_000))
     cfg = RunConfig(gpu_capacity_tokens=w.gpu_capacity_tokens, host_capacity_tokens=host,
                     k=w.k, profile_path=path, decode_ms_per_token=dec,
                     kv_bytes_per_token=float(w.model.kv_bytes_per_token),
                     pcie_bandwidth_bytes_per_ms=pcie * 1e6, stage_interval_ms=stage_ms,
                     seed=w.seed)
-    ng = pool_blocks(w.gpu_capacity_tokens, w.block_tokens, min_doc, 8 * (w.k + 1))
-    nh = pool_blocks(host, w.block_tokens, min_doc, 0)
+    ng = pool_blocks(w.gpu_capacity_tokens, w.block_tokens, sizes.values(), 8 * (w.k + 1))
+    nh = pool_blocks(host, w.block_tokens, sizes.values(), 0)
     s = w.model
     pool = None
     ex = None

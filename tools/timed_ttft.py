@@ -55,7 +55,6 @@ def main():
     path = os.path.join("/tmp", f"{w.shape}_timed_profile.csv")
     save_profile_csv(prof, path)
     trace, sizes = make_stream(w, n_req, rate=rate)
-    min_doc = min(sizes.values())
     floor = w.k * int(w.doc_tokens_mean) + w.prompt_tokens + 64
     tiers = sorted({max(floor, t) for t in (2200, 55_000)})
     rows = []
@@ -64,8 +63,8 @@ def main():
                         k=w.k, profile_path=path, decode_ms_per_token=dec,
                         stage_interval_ms=stage_ms,
                         kv_bytes_per_token=float(w.model.kv_bytes_per_token), seed=w.seed)
-        ng = pool_blocks(cap, w.block_tokens, min_doc, 8 * (w.k + 1))
-        nh = pool_blocks(w.host_capacity_tokens, w.block_tokens, min_doc, 0) or 1
+        ng = pool_blocks(cap, w.block_tokens, sizes.values(), 8 * (w.k + 1))
+        nh = pool_blocks(w.host_capacity_tokens, w.block_tokens, sizes.values(), 0) or 1
         t1 = time.time()
         prof_rep, _ = cache.run_tiered(cfg, trace, sizes, pool=accounting_pool(ng, nh, w.block_tokens))
         s = w.model

@@ -30,8 +30,8 @@ def rope_inv_freq(head_dim: int, theta: float) -> torch.Tensor:
 def apply_rope(x: torch.Tensor, positions: torch.Tensor, theta: float) -> torch.Tensor:
     """Rotate-half RoPE (LLaMA convention) in fp32. x: [T, H, d], positions: [T]."""
     d = x.shape[-1]
-    inv = rope_inv_freq(d, theta)
-    ang = positions.to(torch.float32)[:, None] * inv[None, :]
+    inv = rope_inv_freq(d, theta).to(x.device)
+    ang = positions.to(x.device, torch.float32)[:, None] * inv[None, :]
     cos, sin = ang.cos()[:, None, :], ang.sin()[:, None, :]
     x = x.to(torch.float32)
     x0, x1 = x[..., : d // 2], x[..., d // 2:]
@@ -58,12 +58,15 @@ def prefix_prefill(q: torch.Tensor, pool: torch.Tensor, requests, layer: int,
                    softmax_scale: float | None = None) -> torch.Tensor:
     """q: [T_total, Hq, d] (post-RoPE); requests: [(q_len, q_pos0, blocks, valid)].
 
-    Returns fp32 [T_total, Hq, d]."""
+    Returns fp32 [T_total, Hq, d] on q's device (a CUDA q and pool run this fp32
+    restatement on the GPU: the plain-PyTorch fp32 reference at sizes the host cannot
+    finish in seconds; TF32 must be off)."""
     t_total, hq, d = q.shape
     hkv = pool.shape[3]
     g = hq // hkv
     scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(d)
-    out = torch.zeros((t_total, hq, d), dtype=torch.float32)
+    dev = q.device
+    out = torch.zeros((t_total, hq, d), dtype=torch.float32, device=dev)
     start = 0
     for q_len, q_pos0, blocks, valid in requests:
         k, v = gather_request_kv(pool, layer, blocks, valid)  # [Hkv, S, d]
@@ -73,8 +76,8 @@ def prefix_prefill(q: torch.Tensor, pool: torch.Tensor, requests, layer: int,
         vq = v.repeat_interleave(g, dim=0)
         qr = q[start:start + q_len].to(torch.float32).permute(1, 0, 2)  # [Hq, t, d]
         scores = torch.matmul(qr, kq.transpose(1, 2)) * scale  # [Hq, t, S]
-        qpos = q_pos0 + torch.arange(q_len)
-        kpos = torch.arange(s_len)
+        qpos = q_pos0 + torch.arange(q_len, device=dev)
+        kpos = torch.arange(s_len, device=dev)
         mask = kpos[None, :] > qpos[:, None]
         scores = scores.masked_fill(mask[None], float("-inf"))
         p = torch.softmax(scores, dim=-1)

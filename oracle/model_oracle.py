@@ -23,17 +23,20 @@ def _rms(x, w, eps):
     return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + eps) * w
 
 
-def forward_full(weights, dims, tokens: torch.Tensor) -> torch.Tensor:
-    """weights: the model's dict (any dtype/device); returns fp32 logits [S, vocab]."""
+def forward_full(weights, dims, tokens: torch.Tensor, device="cpu",
+                 last_only: bool = False) -> torch.Tensor:
+    """weights: the model's dict (any dtype/device); returns fp32 logits [S, vocab]
+    ([1, vocab] of the last token with last_only).  device="cuda" runs the same fp32
+    arithmetic on the GPU (TF32 off) for full-size geometries."""
     s = dims.shape
-    f = lambda t: t.detach().to("cpu", torch.float32)
+    f = lambda t: t.detach().to(device, torch.float32)
     S = tokens.shape[0]
-    x = f(weights["emb"])[tokens.cpu()]
-    pos = torch.arange(S)
+    x = f(weights["emb"])[tokens.to(device)]
+    pos = torch.arange(S, device=device)
     qw = s.n_q_heads * s.head_dim
     kw = s.n_kv_heads * s.head_dim
     g = s.n_q_heads // s.n_kv_heads
-    mask = torch.triu(torch.ones(S, S, dtype=torch.bool), 1)
+    mask = torch.triu(torch.ones(S, S, dtype=torch.bool, device=device), 1)
     for lw in weights["layers"]:
         h = _rms(x, f(lw["ln1"]), dims.norm_eps)
         qkv = h @ f(lw["wqkv"])
@@ -49,4 +52,6 @@ def forward_full(weights, dims, tokens: torch.Tensor) -> torch.Tensor:
         h = _rms(x, f(lw["ln2"]), dims.norm_eps)
         gu = h @ f(lw["wgu"])
         x = x + (torch.nn.functional.silu(gu[:, : dims.ffn]) * gu[:, dims.ffn:]) @ f(lw["wdown"])
+    if last_only:
+        x = x[-1:]
     return _rms(x, f(weights["norm"]), dims.norm_eps) @ f(weights["lm_head"])

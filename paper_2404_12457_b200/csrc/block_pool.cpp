@@ -439,8 +439,18 @@ int rcb_node_free_host(rcb_pool* p, int64_t key) {
   return RCB_OK;
 }
 
+// a key repeated in one batch would pass the per-key validation twice and then leak /
+// overwrite its blocks in the mutation loop: rejected before any state changes
+static bool has_duplicate(const int64_t* keys, int32_t n) {
+  std::unordered_set<int64_t> seen;
+  for (int32_t i = 0; i < n; ++i)
+    if (!seen.insert(keys[i]).second) return true;
+  return false;
+}
+
 int rcb_node_swap_out(rcb_pool* p, const int64_t* keys, int32_t n) {
   if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  if (has_duplicate(keys, n)) return set_error(RCB_ERR_ARG, "swap-out: duplicate node key");
   int64_t need = 0;
   for (int32_t i = 0; i < n; ++i) {
     auto it = p->nodes.find(keys[i]);
@@ -464,6 +474,7 @@ int rcb_node_swap_out(rcb_pool* p, const int64_t* keys, int32_t n) {
 
 int rcb_node_swap_in(rcb_pool* p, const int64_t* keys, int32_t n) {
   if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
+  if (has_duplicate(keys, n)) return set_error(RCB_ERR_ARG, "swap-in: duplicate node key");
   int64_t need = 0;
   for (int32_t i = 0; i < n; ++i) {
     auto it = p->nodes.find(keys[i]);

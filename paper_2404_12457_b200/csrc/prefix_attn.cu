@@ -864,21 +864,22 @@ __global__ void __launch_bounds__(kRows)
     if (ml.y > 0.f) mx = fmaxf(mx, ml.x);
   }
   float wsum = 0.f;
-  float wt[32];
-  for (int p = 0; p < np && p < 32; ++p) {
+  for (int p = 0; p < np; ++p) {
     const float2 ml = part_ml[static_cast<int64_t>(slot0 + p) * kRows + row];
-    wt[p] = ml.y > 0.f ? exp2f(ml.x - mx) * ml.y : 0.f;
-    wsum += wt[p];
+    wsum += ml.y > 0.f ? exp2f(ml.x - mx) * ml.y : 0.f;
   }
   const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
   __nv_bfloat16* orow = out + (static_cast<int64_t>(q_start + tok) * n_q_heads + kvh * G + row % G) * HD;
+  // any number of parts: a part's weight is recomputed per 8-column chunk (no per-part array)
   for (int c = 0; c < HD; c += 8) {
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int p = 0; p < np && p < 32; ++p) {
+    for (int p = 0; p < np; ++p) {
+      const float2 ml = part_ml[static_cast<int64_t>(slot0 + p) * kRows + row];
+      if (!(ml.y > 0.f)) continue;
       const float4* src = reinterpret_cast<const float4*>(
           part_o + (static_cast<int64_t>(slot0 + p) * kRows + row) * HD + c);
       const float4 a = src[0], b = src[1];
-      const float w = wt[p] * inv;
+      const float w = exp2f(ml.x - mx) * ml.y * inv;
       acc[0] += w * a.x; acc[1] += w * a.y; acc[2] += w * a.z; acc[3] += w * a.w;
       acc[4] += w * b.x; acc[5] += w * b.y; acc[6] += w * b.z; acc[7] += w * b.w;
     }

@@ -248,7 +248,7 @@ class HotPath:
                                   block_tokens=self.block_tokens, n_layers=s.n_layers,
                                   n_kv_heads=s.n_kv_heads, head_dim=s.head_dim, layer=layer,
                                   rope_theta=s.rope_theta, n_q_heads=s.n_q_heads, rope=rope,
-                                  stream=stream)
+                                  max_pos=d["attn"].max_pos, stream=stream)
             if events is not None:
                 events[layer][0].record()
             kernels.prefix_prefill(q, o, d["attn"], base, self.num_gpu_blocks,

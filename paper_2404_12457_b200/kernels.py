@@ -59,11 +59,13 @@ def kv_write_rope(q, k: torch.Tensor, v: torch.Tensor, q_out, positions: torch.T
                   slots: torch.Tensor, pool_base: int, *, block_tokens: int, n_layers: int,
                   n_kv_heads: int, head_dim: int, layer: int, rope_theta: float,
                   n_q_heads: int | None = None, rope: torch.Tensor | None = None,
-                  stream=None) -> None:
+                  max_pos: int | None = None, stream=None) -> None:
     """RoPE q,k then scatter k,v into the pool (q/k/v may be strided row views).
     q = q_out = None: K/V only (Q is rotated inside prefix_prefill).  With ``rope`` (an
-    rcb_rope_table covering every position) cos/sin are read from it instead of being
-    recomputed per token (identical values)."""
+    rcb_rope_table) cos/sin are read from it instead of being recomputed per token
+    (identical values); ``max_pos`` (exclusive bound of ``positions``, e.g.
+    AttnPlan.max_pos) is then required and must be covered by the table: the kernel
+    indexes the table by position without a bounds check."""
     n_tokens = k.shape[0]
     if n_q_heads is None:
         n_q_heads = q_out.shape[1]
@@ -73,6 +75,9 @@ def kv_write_rope(q, k: torch.Tensor, v: torch.Tensor, q_out, positions: torch.T
     if rope is not None:  # cos/sin from an rcb_rope_table (covering every position)
         if rope.dtype != torch.float32 or rope.shape[1] * 2 != head_dim:
             raise ValueError(f"rope table {tuple(rope.shape)} does not match head_dim {head_dim}")
+        if max_pos is None or rope.shape[0] < max_pos:
+            raise ValueError(f"rope table of {rope.shape[0]} rows must cover positions < max_pos "
+                             f"({max_pos}; pass the positions' exclusive bound)")
         check(load().rcb_kv_write_rope_table(
             _dev_ptr(q) if q is not None else None, q.stride(0) if q is not None else 0,
             _dev_ptr(k), _dev_ptr(v), k.stride(0),

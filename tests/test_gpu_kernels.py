@@ -178,6 +178,8 @@ ATTN_CASES = [
     (128, 32, 8, 64, 1, [([1020], [32])]),
     (128, 32, 32, 64, 1, [([2048], [1]), ([500], [3])]),
     (64, 8, 4, 16, 2, [([300, 200], [2])]),
+    # MQA decode over a long context: 94 KV tiles -> 47 split-KV parts (> 32) in one group
+    (128, 8, 1, 64, 1, [([12000], [1])]),
 ]
 
 
@@ -206,6 +208,20 @@ def test_prefix_prefill_matches_oracle(hd, hq, hkv, bt, L, reqs, split_kv):
         ref = attn_oracle.prefix_prefill(q.cpu().float(), pool.cpu(), requests, layer)
         err = (out.cpu().float() - ref).abs().max().item()
         assert err <= ATTN_ATOL, f"layer {layer}: max |err| {err}"
+
+
+def test_rope_table_must_cover_the_positions():
+    pool = torch.zeros((4, 1, 2, 1, 16, 64), dtype=torch.bfloat16, device="cuda")
+    kv = torch.zeros((3, 64), dtype=torch.bfloat16, device="cuda")
+    pos = torch.tensor([0, 1, 40], dtype=torch.int32, device="cuda")
+    slots = torch.tensor([0, 1, 2], dtype=torch.int32, device="cuda")
+    table = kernels.rope_table(32, 64, 1e4)
+    kw = dict(block_tokens=16, n_layers=1, n_kv_heads=1, head_dim=64, layer=0, rope_theta=1e4,
+              n_q_heads=1, rope=table)
+    with pytest.raises(ValueError):
+        kernels.kv_write_rope(None, kv, kv, None, pos, slots, pool.data_ptr(), max_pos=41, **kw)
+    with pytest.raises(ValueError):
+        kernels.kv_write_rope(None, kv, kv, None, pos, slots, pool.data_ptr(), **kw)
 
 
 def test_split_kv_plan_splits_small_split_only_launches():
@@ -316,7 +332,7 @@ def test_kv_write_rope_table_is_bit_identical(with_q):
         q_out = torch.zeros((T, hq, hd), dtype=torch.bfloat16, device="cuda") if with_q else None
         kernels.kv_write_rope(q, k, v, q_out, pos, slots, pool.data_ptr(), block_tokens=bt,
                               n_layers=L, n_kv_heads=hkv, head_dim=hd, layer=1, rope_theta=theta,
-                              n_q_heads=hq, rope=rope)
+                              n_q_heads=hq, rope=rope, max_pos=int(pos.max()) + 1)
         torch.cuda.synchronize()
         outs.append((pool, q_out))
     assert torch.equal(outs[0][0].view(torch.int16), outs[1][0].view(torch.int16))

@@ -251,7 +251,7 @@ def bench_attn():
             fn = lambda: kernels.kv_write_rope(qq, k, v, qo, pos_t, slots, pool.data_ptr(),
                                                block_tokens=bt, n_layers=L, n_kv_heads=hkv,
                                                head_dim=hd, layer=1, rope_theta=1e6, n_q_heads=hq,
-                                               rope=tab)
+                                               rope=tab, max_pos=int(pos_t.max()) + 1)
             med, best = timed(fn)
             nbytes = T * hd * 2 * (2 * hkv * 2 + (2 * hq if qq is not None else 0))
             emit(kind="kv_write_rope", mode=mode, case=name, ms=med, gbs=nbytes / med / 1e6)

@@ -120,7 +120,9 @@ class PrefillModel:
             mlp = kernels.silu_mul(h @ lw["wgu"], stream=stream) @ lw["wdown"]
             nxt = layers[layer + 1]["ln1"] if layer + 1 < len(layers) else self.w["norm"]
             h = kernels.rmsnorm_residual(x, mlp, nxt, d.norm_eps, stream=stream)
-        return (h[last_rows] @ self.w["lm_head"]).float()
+        # logits leave the GEMM in fp32 (cuBLAS accumulates in fp32 either way): a bf16
+        # output would add a rounding of up to |logit| * 2^-9 on top of the activations'
+        return torch.mm(h[last_rows], self.w["lm_head"], out_dtype=torch.float32)
 
 
 def suffix_slots(blocks, valid, n_prefix_blocks: int, block_tokens: int, alpha: int):

@@ -452,6 +452,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     int c = 0;   // tiles processed (S_w / P_w phase)
     int oc = 0;  // items with a non-empty Q_w (L slot phase)
     int st = 0;  // KV step (meta ring)
+    // Every first-half PV commits kPVDone; a tile that rescaled in chunk 1 consumed that
+    // phase already, the others consume it after the next S-full (free: that PV precedes
+    // the next QK_w in MMA order) or at exit, so every arrival is waited (synccheck)
+    bool pv_pending = false;
     for (int idx = blockIdx.x; idx < n_work; idx += gridDim.x) {
       const Item it = load_item(work, idx);
       const int n = it.n();
@@ -480,6 +484,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool tr = (threadIdx.x & 127) == 0 && quad == 0;
         if (tr) TRACE(c, 4 * wg + 0);
         mbar_wait(&bar[kSFull0 + wg], c & 1);
+        if (pv_pending) mbar_wait(&bar[kPVDone0 + wg], (c - 1) & 1);
+        pv_pending = true;
         if (tr) TRACE(c, 4 * wg + 1);
         tc_fence_after();
         const bool masked = !all_valid || max_pos > qp;
@@ -533,6 +539,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // first-half PV, so let that retire and rescale O_w as a whole instead
             if (ch == 1) {
               mbar_wait(&bar[kPVDone0 + wg], c & 1);
+              pv_pending = false;
               tc_fence_after();
             }
             if (ch == 1 || j > it.first(wg)) {
@@ -591,6 +598,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++oc;
       }
     }
+    if (pv_pending) mbar_wait(&bar[kPVDone0 + wg], (c - 1) & 1);
   } else if (warp >= 8) {
 #if RCB_REG_EP > 128
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(RCB_REG_EP));

@@ -23,6 +23,24 @@ def _rms(x, w, eps):
     return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + eps) * w
 
 
+def _moe(h, lw, dims, f):
+    """Mixtral sparse FFN (the published routing: softmax over the top-k router logits,
+    weighted sum of those experts' SwiGLU outputs), fp32, dense per-expert loop."""
+    logits = h @ f(lw["router"])
+    top_v, top_i = torch.topk(logits, dims.top_k, dim=-1)
+    wts = torch.softmax(top_v, dim=-1)
+    out = torch.zeros_like(h)
+    for e in range(dims.n_experts):
+        sel = (top_i == e)
+        rows = sel.any(-1).nonzero().reshape(-1)
+        if rows.numel() == 0:
+            continue
+        gu = h[rows] @ f(lw["wgu"][e])
+        y = (torch.nn.functional.silu(gu[:, : dims.ffn]) * gu[:, dims.ffn:]) @ f(lw["wdown"][e])
+        out[rows] += y * (wts[rows] * sel[rows]).sum(-1, keepdim=True)
+    return out
+
+
 def forward_full(weights, dims, tokens: torch.Tensor, device="cpu",
                  last_only: bool = False) -> torch.Tensor:
     """weights: the model's dict (any dtype/device); returns fp32 logits [S, vocab]
@@ -50,8 +68,11 @@ def forward_full(weights, dims, tokens: torch.Tensor, device="cpu",
         o = torch.einsum("hts,shd->thd", torch.softmax(sc, -1), v).reshape(S, qw)
         x = x + o @ f(lw["wo"])
         h = _rms(x, f(lw["ln2"]), dims.norm_eps)
-        gu = h @ f(lw["wgu"])
-        x = x + (torch.nn.functional.silu(gu[:, : dims.ffn]) * gu[:, dims.ffn:]) @ f(lw["wdown"])
+        if getattr(dims, "n_experts", 0):
+            x = x + _moe(h, lw, dims, f)
+        else:
+            gu = h @ f(lw["wgu"])
+            x = x + (torch.nn.functional.silu(gu[:, : dims.ffn]) * gu[:, dims.ffn:]) @ f(lw["wdown"])
     if last_only:
         x = x[-1:]
     return _rms(x, f(weights["norm"]), dims.norm_eps) @ f(weights["lm_head"])

@@ -31,6 +31,8 @@ class ModelDims:
     ffn: int
     vocab: int
     norm_eps: float = 1e-5
+    n_experts: int = 0  # > 0: sparse MoE FFN (Mixtral), top_k experts per token
+    top_k: int = 2
 
 
 DIMS = {
@@ -38,6 +40,9 @@ DIMS = {
     "mistral-7b": ModelDims(SHAPES["mistral-7b"], 4096, 14336, 32000),
     "llama2-7b": ModelDims(SHAPES["llama2-7b"], 4096, 11008, 32000),
     "llama2-13b": ModelDims(SHAPES["llama2-13b"], 5120, 13824, 32000),
+    # configs[4]: Mixtral-8x7B (32 layers, GQA 32/8, 8 experts of FFN 14336, top-2;
+    # ~93 GB of bf16 weights, one B200)
+    "mixtral-8x7b": ModelDims(SHAPES["mixtral-8x7b"], 4096, 14336, 32000, n_experts=8, top_k=2),
 }
 
 
@@ -52,17 +57,26 @@ def init_weights(dims: ModelDims, seed: int = 0, device="cuda", dtype=torch.bflo
         t = torch.randn((rows, cols), generator=g, device=gen_dev) * (scale / rows ** 0.5)
         return t.to(device=device, dtype=dtype)
 
+    def experts(rows, cols):  # [E, rows, cols], one matrix per expert
+        return torch.stack([w(rows, cols) for _ in range(dims.n_experts)])
+
     qkv = (s.n_q_heads + 2 * s.n_kv_heads) * s.head_dim
     layers = []
     for _ in range(s.n_layers):
-        layers.append({
+        lw = {
             "ln1": (1.0 + 0.1 * torch.randn(dims.d_model, generator=g, device=gen_dev)).to(device, dtype),
             "wqkv": w(dims.d_model, qkv),
             "wo": w(s.n_q_heads * s.head_dim, dims.d_model),
             "ln2": (1.0 + 0.1 * torch.randn(dims.d_model, generator=g, device=gen_dev)).to(device, dtype),
-            "wgu": w(dims.d_model, 2 * dims.ffn),
-            "wdown": w(dims.ffn, dims.d_model),
-        })
+        }
+        if dims.n_experts:
+            lw["router"] = w(dims.d_model, dims.n_experts)
+            lw["wgu"] = experts(dims.d_model, 2 * dims.ffn)
+            lw["wdown"] = experts(dims.ffn, dims.d_model)
+        else:
+            lw["wgu"] = w(dims.d_model, 2 * dims.ffn)
+            lw["wdown"] = w(dims.ffn, dims.d_model)
+        layers.append(lw)
     return {
         "emb": (torch.randn((dims.vocab, dims.d_model), generator=g, device=gen_dev)).to(device, dtype),
         "layers": layers,
@@ -117,12 +131,72 @@ class PrefillModel:
                                    rope=self.rope, n_q_heads=s.n_q_heads, stream=stream)
             h = kernels.rmsnorm_residual(x, attn.view(T, qw) @ lw["wo"], lw["ln2"], d.norm_eps,
                                          stream=stream)
-            mlp = kernels.silu_mul(h @ lw["wgu"], stream=stream) @ lw["wdown"]
+            if d.n_experts:
+                mlp = moe_ffn(h, lw, d, stream=stream)
+            else:
+                mlp = kernels.silu_mul(h @ lw["wgu"], stream=stream) @ lw["wdown"]
             nxt = layers[layer + 1]["ln1"] if layer + 1 < len(layers) else self.w["norm"]
             h = kernels.rmsnorm_residual(x, mlp, nxt, d.norm_eps, stream=stream)
         # logits leave the GEMM in fp32 (cuBLAS accumulates in fp32 either way): a bf16
         # output would add a rounding of up to |logit| * 2^-9 on top of the activations'
-        return torch.mm(h[last_rows], self.w["lm_head"], out_dtype=torch.float32)
+        return _mm_f32(h[last_rows], self.w["lm_head"])
+
+
+def _mm_f32(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """bf16 GEMM with an fp32 output (cuBLAS accumulates in fp32; no bf16 output rounding)."""
+    if a.is_cuda:
+        return torch.mm(a, b, out_dtype=torch.float32)
+    return a.float() @ b.float()
+
+
+_GROUPED_MM = None  # torch._grouped_mm usable on this device (probed on first use)
+
+
+def _grouped(x: torch.Tensor, w3: torch.Tensor, offs: torch.Tensor) -> torch.Tensor:
+    """rows [offs[e-1], offs[e]) of x times w3[e]: one grouped GEMM (no host sync, CUDA-graph
+    capturable); a per-expert loop over library GEMMs where the grouped kernel is missing."""
+    global _GROUPED_MM
+    if _GROUPED_MM is not False:
+        try:
+            y = torch._grouped_mm(x, w3, offs=offs)
+            _GROUPED_MM = True
+            return y
+        except (RuntimeError, NotImplementedError, AttributeError):
+            if _GROUPED_MM:
+                raise
+            _GROUPED_MM = False
+    ends = offs.tolist()
+    out = torch.empty((x.shape[0], w3.shape[2]), dtype=x.dtype, device=x.device)
+    lo = 0
+    for e, hi in enumerate(ends):
+        if hi > lo:
+            torch.mm(x[lo:hi], w3[e], out=out[lo:hi])
+        lo = hi
+    return out
+
+
+def moe_ffn(h: torch.Tensor, lw, dims: ModelDims, stream=None) -> torch.Tensor:
+    """Mixtral sparse FFN on bf16 rows h [T, d]: router logits in fp32, top-k experts per
+    token, their softmax-renormalised weights; the T*k (token, expert) rows are sorted by
+    expert and run through per-expert gate/up and down GEMMs (grouped), then combined
+    into bf16 [T, d].  The combine adds the k fp32 contributions to a zero row, which is
+    order-independent (two addends), so the result is deterministic."""
+    T = h.shape[0]
+    k = dims.top_k
+    logits = _mm_f32(h, lw["router"])
+    top_v, top_i = torch.topk(logits, k, dim=-1)
+    wts = torch.softmax(top_v, dim=-1).reshape(-1)
+    flat = top_i.reshape(-1)
+    order = torch.argsort(flat, stable=True)
+    tok = order // k
+    counts = torch.zeros(dims.n_experts, dtype=torch.int64, device=h.device)
+    counts.scatter_add_(0, flat, torch.ones_like(flat))  # (bincount would sync on its max)
+    offs = torch.cumsum(counts, 0).to(torch.int32)
+    gu = _grouped(h[tok], lw["wgu"], offs)
+    y = _grouped(kernels.silu_mul(gu, stream=stream), lw["wdown"], offs)
+    out = torch.zeros((T, h.shape[1]), dtype=torch.float32, device=h.device)
+    out.index_add_(0, tok, y.float() * wts[order][:, None])
+    return out.to(h.dtype)
 
 
 def suffix_slots(blocks, valid, n_prefix_blocks: int, block_tokens: int, alpha: int):

@@ -33,6 +33,12 @@ from ragsim.cost_model import DEFAULT_GRID, CostProfile  # noqa: E402
 BETA_GRID = (0, 1, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096)
 
 
+def _grouped_ok() -> bool:
+    from . import model as _model
+
+    return bool(_model._GROUPED_MM)
+
+
 def decode_ms_per_token(profile, context_tokens: int) -> float:
     """One decode step of one request = a one-token prefill over its cached context:
     the model forward with the same GEMMs and the prefix-prefill kernel as the paged
@@ -84,7 +90,9 @@ def measure_profile(shape: str = "mistral-7b", alpha_grid=DEFAULT_GRID, beta_gri
             fn = lambda: model.prefill(tok, pos_t, slot_t, plan, last)
             fn()
             fn()
-            if cuda_graph:
+            # a MoE model without the grouped GEMM syncs on its expert offsets: eager
+            from . import model as _model
+            if cuda_graph and (not dims.n_experts or _model._GROUPED_MM):
                 # one graph per (alpha, beta): every layer's GEMMs and rcb kernels
                 # replay without per-launch host overhead
                 graph = torch.cuda.CUDAGraph()
@@ -115,5 +123,6 @@ def measure_profile(shape: str = "mistral-7b", alpha_grid=DEFAULT_GRID, beta_gri
     prof = CostProfile(tuple(alpha_grid), tuple(beta_grid), tuple(times))
     info = {"shape": shape, "block_tokens": block_tokens, "reps": reps,
             "weights": "random-init bf16 (seeded)",
-            "timing": "CUDA events, median" + (", CUDA-graph replay" if cuda_graph else ", eager")}
+            "timing": "CUDA events, median" + (", CUDA-graph replay" if cuda_graph and (
+                not dims.n_experts or _grouped_ok()) else ", eager")}
     return prof, info

@@ -36,6 +36,8 @@ class TimedEngine(TieredEngine):
     def __init__(self, *args, executor, **kwargs) -> None:
         super().__init__(*args, executor=executor, **kwargs)
         self.measured: list[tuple[int, int, int, float, float]] = []  # (req, alpha, beta, profile ms, measured ms)
+        self.skipped_chunks = 0  # chunks of terminated speculations that never ran
+        self.planned_chunks = 0  # chunks of every chunked admission (run + skipped)
         # (req, modeled transfer ms, charged transfer ms, charged prefill ms) per admission
         self.critical: list[tuple[int, float, float, float]] = []
 
@@ -56,13 +58,39 @@ class TimedEngine(TieredEngine):
             # the swap-in was executed and is inside the measured time (serial or
             # layer-pipelined); only its exposed part remains on the critical path
             gen.transfer_ms = float(self.executor.last_transfer_ms)
-        total = gen.transfer_ms + gen.prefill_ms
-        chunks = max(1, math.ceil(total / self.config.prefill_chunk_ms)) if total > 0 else 1
-        gen.chunk_ms = total / chunks
-        gen.chunks_left = chunks
+        if getattr(gen, "exec_state", None) is not None:
+            # chunked execution (simulator.py:507-510): the executor ran chunk 0 of the
+            # reference's chunk count; each later chunk runs at its iteration boundary
+            # (_on_prefill_iteration), so a terminated speculation stops launching
+            gen.chunk_ms = gen.transfer_ms + gen.prefill_ms
+        else:
+            total = gen.transfer_ms + gen.prefill_ms
+            chunks = max(1, math.ceil(total / self.config.prefill_chunk_ms)) if total > 0 else 1
+            gen.chunk_ms = total / chunks
+            gen.chunks_left = chunks
+        if getattr(gen, "exec_state", None) is not None:
+            gen.exec_state["measured_idx"] = len(self.measured)
+            self.planned_chunks += gen.chunks_left
         self.measured.append((gen.request.id, gen.alpha, gen.beta, modeled, gen.prefill_ms))
         self.critical.append((gen.request.id, modeled_transfer, gen.transfer_ms, gen.prefill_ms))
         self._schedule(self._now + gen.chunk_ms, kind, rid, payload)
+
+    def _on_prefill_iteration(self, gen) -> None:
+        """simulator.py:408-425 with real chunks: at a boundary of a chunked generation that
+        goes on (not terminated, chunks left), the next chunk runs on the GPU and its
+        measured time is the next iteration's length.  ragsim's bookkeeping (executed_ms +=
+        the finished chunk) is kept by pre-compensating executed_ms."""
+        st = getattr(gen, "exec_state", None)
+        if st is not None and not gen.terminated and gen.chunks_left > 1:
+            nxt = float(self.executor.run_chunk(gen, st["n"] - gen.chunks_left + 1))
+            gen.executed_ms += gen.chunk_ms - nxt
+            gen.chunk_ms = nxt
+            gen.prefill_ms += nxt
+            self.measured[st["measured_idx"]] = self.measured[st["measured_idx"]][:4] + (
+                gen.prefill_ms,)
+        elif st is not None and gen.terminated and gen.chunks_left > 1:
+            self.skipped_chunks += gen.chunks_left - 1  # never launched
+        super()._on_prefill_iteration(gen)
 
 
 def run_timed(config, trace, sizes, *, pool, executor, stage_provider=None):
@@ -101,13 +129,18 @@ class ModelExecutor:
     timed region in every mode (the reference keeps them off the critical path)."""
 
     def __init__(self, pool, shape: str, *, seed: int = 0, device="cuda", swap_in: str = "modeled",
-                 layers_per_group: int = 4) -> None:
+                 layers_per_group: int = 4, chunked: bool = False, dims=None) -> None:
         if swap_in not in ("modeled", "serial", "layered"):
             raise ValueError(f"swap_in must be modeled, serial or layered, not {swap_in!r}")
         self.swap_in = swap_in
         self.layers_per_group = layers_per_group
         self.last_transfer_ms = None
-        self.dims = DIMS[shape]
+        self.dims = dims if dims is not None else DIMS[shape]
+        # chunked: run the suffix in the reference's chunk count (simulator.py:507-510),
+        # one chunk per iteration boundary (TimedEngine._on_prefill_iteration)
+        self.chunked = chunked
+        self.chunks_run = 0
+        self.last_logits = None
         self.pool = pool
         self.w = init_weights(self.dims, seed=seed, device=device)
         self.model = PrefillModel(self.dims, self.w, block_tokens=pool.block_tokens,
@@ -128,15 +161,42 @@ class ModelExecutor:
         tok = torch.from_numpy(np.concatenate(parts)).to(self.device)
         n_prefix = sum(-(-n.size // bt) for n in gen.matched_nodes)
         slots, pos = suffix_slots(blocks, valid, n_prefix, bt, alpha)
-        plan = kernels.AttnPlan([(beta, alpha, blocks, valid)], block_tokens=bt,
+        idx = kernels._upload(np.asarray(pos + slots, dtype=np.int32), self.device)
+        n = max(1, min(int(gen.chunks_left), beta)) if self.chunked else 1
+        st = {"tok": tok, "pos": idx[:beta], "slots": idx[beta:], "blocks": list(blocks),
+              "valid": list(valid), "alpha": alpha, "beta": beta, "n": n,
+              "cuts": [round(c * beta / n) for c in range(n + 1)]}
+        if self.chunked:
+            gen.exec_state = st
+            gen.chunks_left = n
+        self.last_ms = self._run(st, 0, first=True)
+        self.last_transfer_ms = None if self.swap_in == "modeled" else 0.0
+
+    def run_chunk(self, gen, c: int) -> float:
+        """Chunk c (> 0) of a chunked generation: its tokens over the cached prefix plus the
+        earlier chunks' pages (written by their K/V writes)."""
+        return self._run(gen.exec_state, c, first=False)
+
+    def _run(self, st, c: int, first: bool) -> float:
+        lo, hi = st["cuts"][c], st["cuts"][c + 1]
+        alpha = st["alpha"]
+        # block table truncated to the tokens this chunk may attend: alpha + hi
+        blocks, valid, need = [], [], alpha + hi
+        for b, v in zip(st["blocks"], st["valid"]):
+            if need <= 0:
+                break
+            blocks.append(b)
+            valid.append(min(v, need))
+            need -= v
+        plan = kernels.AttnPlan([(hi - lo, alpha + lo, blocks, valid)],
+                                block_tokens=self.pool.block_tokens,
                                 n_q_heads=self.dims.shape.n_q_heads,
                                 n_kv_heads=self.dims.shape.n_kv_heads, device=self.device)
-        idx = kernels._upload(np.asarray(pos + slots, dtype=np.int32), self.device)
-        last = torch.tensor([beta - 1], device=self.device)
+        last = torch.tensor([hi - lo - 1], device=self.device)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         fence = None
-        if self.swap_in == "modeled":
+        if not first or self.swap_in == "modeled":
             self.pool.fence_into(self.stream)  # swap-ins landed before the prefill reads them
             e0.record(self.stream)
         else:
@@ -148,12 +208,13 @@ class ModelExecutor:
                 fence = lambda layer: self.pool.fence_layer(layer, self.stream)  # noqa: E731
             else:
                 self.pool.fence_into(self.stream)
-        self.model.prefill(tok, idx[:beta], idx[beta:], plan, last, layer_fence=fence)
+        self.last_logits = self.model.prefill(st["tok"][lo:hi], st["pos"][lo:hi],
+                                              st["slots"][lo:hi], plan, last, layer_fence=fence)
         e1.record(self.stream)
         self.pool.wait_for(self.stream)  # later swap-outs read the finished pages
         e1.synchronize()
-        self.last_ms = e0.elapsed_time(e1)
-        self.last_transfer_ms = None if self.swap_in == "modeled" else 0.0
+        self.chunks_run += 1
+        return e0.elapsed_time(e1)
 
 
 class ProfileExecutor:

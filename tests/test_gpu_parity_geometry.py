@@ -1,6 +1,7 @@
 """Parity at the geometries the bench runs ("pin parity at the configs you bench").
 
-(b) Cached-prefix prefill logits at Mistral-7B (GQA-4) and LLaMA2-7B (MHA) geometry: head
+(b) Cached-prefix prefill logits at Mistral-7B (GQA-4), LLaMA2-7B (MHA) and Mixtral-8x7B
+    (GQA-4, 8-expert top-2 MoE FFN) geometry: head
     dim 128, 64-token blocks, full hidden size / FFN / vocab, 2 layers, 512-token documents
     (plus a ragged 300-token one for node tails), against the fp32 full-recompute oracle:
     max |logit error| <= 1e-2 (north star).
@@ -39,7 +40,7 @@ def _no_tf32():
     torch.backends.cuda.matmul.allow_tf32 = old
 
 
-@pytest.mark.parametrize("model", ["mistral-7b", "llama2-7b"])
+@pytest.mark.parametrize("model", ["mistral-7b", "llama2-7b", "mixtral-8x7b"])
 def test_cached_prefix_logits_at_bench_geometry(model):
     full = DIMS[model]
     shape = dataclasses.replace(full.shape, name=model + "-2l", n_layers=2)

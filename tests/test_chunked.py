@@ -20,13 +20,13 @@ from paper_2404_12457_b200._ragsim import ragsim_available
 pytestmark = pytest.mark.skipif(not ragsim_available(), reason="ragsim not importable")
 
 
-def _dsp_desk(chunk_ms):
+def _dsp_desk(chunk_ms, stage_ms=50.0):
     from ragsim.config import RunConfig
 
     from tests.golden.make_golden import DESK, desk_trace, pool_geometry
 
     trace, sizes = desk_trace(seed=0, duration_s=300.0, rate=0.25, pool=300)
-    cfg = RunConfig(host_capacity_tokens=32768, stage_count=4, stage_interval_ms=50.0,
+    cfg = RunConfig(host_capacity_tokens=32768, stage_count=4, stage_interval_ms=stage_ms,
                     convergence_stage=2, prefill_chunk_ms=chunk_ms, dsp=True, seed=0,
                     validate=True, **DESK)
     return cfg, trace, sizes, pool_geometry(cfg, sizes)
@@ -128,7 +128,9 @@ def test_terminated_speculations_launch_fewer_chunks():
     from paper_2404_12457_b200.pool import BlockPool
     from paper_2404_12457_b200.timed import ModelExecutor, run_timed
 
-    cfg, trace, sizes, (ng, nh) = _dsp_desk(chunk_ms=5.0)
+    # B200 runs the tiny model's chunks in ~0.1-0.3 ms: retrieval stages 0.25 ms apart so that
+    # stale speculations are terminated while their prefill is still running
+    cfg, trace, sizes, (ng, nh) = _dsp_desk(chunk_ms=5.0, stage_ms=0.25)
     pool = BlockPool(ng, nh, block_tokens=16, n_layers=2, n_kv_heads=4, head_dim=64)
     ex = ModelExecutor(pool, "tiny", chunked=True)
     rep, engine = run_timed(cfg, trace, sizes, pool=pool, executor=ex)

@@ -129,7 +129,8 @@ class ModelExecutor:
     timed region in every mode (the reference keeps them off the critical path)."""
 
     def __init__(self, pool, shape: str, *, seed: int = 0, device="cuda", swap_in: str = "modeled",
-                 layers_per_group: int = 4, chunked: bool = False, dims=None) -> None:
+                 layers_per_group: int = 4, chunked: bool = False, dims=None,
+                 weights=None) -> None:
         if swap_in not in ("modeled", "serial", "layered"):
             raise ValueError(f"swap_in must be modeled, serial or layered, not {swap_in!r}")
         self.swap_in = swap_in
@@ -142,7 +143,9 @@ class ModelExecutor:
         self.chunks_run = 0
         self.last_logits = None
         self.pool = pool
-        self.w = init_weights(self.dims, seed=seed, device=device)
+        # weights may be shared across executors (one random-init model, many pools)
+        self.w = weights if weights is not None else init_weights(self.dims, seed=seed,
+                                                                 device=device)
         self.model = PrefillModel(self.dims, self.w, block_tokens=pool.block_tokens,
                                   num_pool_blocks=pool.num_gpu_blocks, pool_base=pool.gpu_base)
         self.stream = torch.cuda.current_stream()

@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--swap-mode", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ttft", action="store_true")
+    ap.add_argument("--no-timed", action="store_true",
+                    help="skip the hardware-in-the-loop TTFT / req/s curves")
     # multi-rank smoke on a single GPU (all ranks on cuda:0, gloo, small tier)
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--single-device", action="store_true")
@@ -349,7 +351,8 @@ def run_ours(args, dist: Dist):
     if dist.rank == 0 and not args.no_ttft:
         del corpus, retr, qkv, q_rot, out
         torch.cuda.empty_cache()
-        ttft = measure_ttft(w, swap, stage_ms=(sum(scan_ms) / max(1, len(scan_ms))) / w.n_stages)
+        ttft = measure_ttft(w, swap, stage_ms=(sum(scan_ms) / max(1, len(scan_ms))) / w.n_stages,
+                            timed_on=not args.no_timed)
 
     result = None
     if dist.rank == 0:
@@ -415,7 +418,57 @@ def run_ours(args, dist: Dist):
     return result
 
 
-def measure_ttft(w, swap, stage_ms: float) -> dict:
+def measure_timed(w, qw, prof, decode_ms, stage_ms, pcie) -> dict:
+    """Hardware-in-the-loop curves (every admitted prefill executed on the GPU, TimedEngine):
+    TTFT vs hit rate over 4 GPU tiers and req/s at the 5x TTFT SLO on the repeated-question
+    variant of this workload, plus configs[2] (LLaMA2-7B top-5, two tiers) with real
+    layer-pipelined swaps."""
+    import tempfile
+
+    from ragsim.cost_model import save_profile_csv
+
+    from paper_2404_12457_b200.timed_curves import (TimedRunner, timed_slo_throughput,
+                                                    timed_ttft_curve)
+    from paper_2404_12457_b200.workloads import WORKLOADS
+
+    out = {"engine": "TimedEngine: ragsim decisions/queue/DSP/virtual clock; every admitted "
+                     "prefill run on the GPU (random-init model: cuBLAS GEMMs + rcb kernels on "
+                     "its block table) and its CUDA-event time advances the clock"}
+    t0 = time.perf_counter()
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "profile.csv")
+        save_profile_csv(prof, path)
+        if qw is not None:
+            floor = qw.k * int(qw.doc_tokens_mean) + qw.prompt_tokens + 64
+            tiers = sorted({max(floor, t) for t in (2200, 55_000, 220_000, 440_000)})
+            runner = TimedRunner(qw, max(tiers), qw.host_capacity_tokens)
+            kw = dict(prof_path=path, dec_ms=decode_ms, stage_ms=stage_ms, pcie_gbs=pcie)
+            out["vs_hit_rate"] = {"workload": qw.name, "requests": 400, "rate_req_s": 2.0,
+                                  "points": timed_ttft_curve(runner, tiers, n_requests=400, **kw)}
+            out["req_per_s_at_5x_slo"] = {
+                "workload": qw.name, "how": "ragsim's measure_throughput bisection "
+                "(simulator.py:648-681), every probe a timed run",
+                "points": [timed_slo_throughput(runner, cap, n_requests=300, **kw)
+                           for cap in (tiers[0], tiers[-1])]}
+            runner.close()
+    c2 = WORKLOADS["llama2-7b-top5-qpool"]
+    c2_prof = os.path.join(ROOT, "profiles", f"{c2.shape}_b200_profile.csv")
+    if os.path.exists(c2_prof):
+        info = json.load(open(c2_prof.replace(".csv", ".json")))
+        runner = TimedRunner(c2, c2.gpu_capacity_tokens, c2.host_capacity_tokens,
+                             swap_in="layered")
+        pts = timed_ttft_curve(runner, [c2.gpu_capacity_tokens], prof_path=c2_prof,
+                               dec_ms=float(info["decode_ms_per_token"]["2592"]),
+                               stage_ms=stage_ms, pcie_gbs=pcie, n_requests=240, rate=1.0)
+        runner.close()
+        out["configs2_two_tier"] = {"workload": c2.name, "gpu_tier_tokens": c2.gpu_capacity_tokens,
+                                    "host_tier_tokens": c2.host_capacity_tokens,
+                                    "swap_in": "layer-pipelined (executed)", **pts[0]}
+    out["seconds"] = round(time.perf_counter() - t0, 1)
+    return out
+
+
+def measure_ttft(w, swap, stage_ms: float, timed_on: bool = True) -> dict:
     """p50 TTFT on B200 costs: measure T(alpha, beta) of the real prefill (our kernels +
     cuBLAS GEMMs, CUDA-graph replay), then run the reference engine (ragsim, decisions
     unchanged) on this workload and on its repeated-question variant across GPU tiers."""
@@ -446,9 +499,10 @@ def measure_ttft(w, swap, stage_ms: float) -> dict:
                              host_tier=qw.host_capacity_tokens, pcie_gbs=pcie,
                              decode_ms_per_token=decode_ms)
         slo_s = time.perf_counter() - t1
+    timed = measure_timed(w, qw, prof, decode_ms, stage_ms, pcie) if timed_on else None
     idx = {(a, b): prof.times[i][j] for i, a in enumerate(prof.alpha_grid)
            for j, b in enumerate(prof.beta_grid)}
-    return {"p50_ttft_ms": own["p50_ttft_ms"], "mean_ttft_ms": own["mean_ttft_ms"],
+    return {"timed": timed, "p50_ttft_ms": own["p50_ttft_ms"], "mean_ttft_ms": own["mean_ttft_ms"],
             "doc_hit_rate": own["doc_hit_rate"], "engine": "ragsim SimulationEngine (TieredEngine) "
             "on the B200-measured prefill profile and decode step, rate 2 req/s, 2000 requests",
             "retrieval_stage_ms": round(stage_ms, 4),

@@ -91,3 +91,28 @@ def test_timed_engine_executes_swap_ins(mode):
     assert all(t == 0.0 for _, _, t, _ in engine.critical)
     assert any(mt > 0 for _, mt, _, _ in engine.critical)  # some admissions had host hits
     pool.close()
+
+
+@pytest.mark.gpu
+def test_timed_curves_and_slo_throughput_tiny():
+    """bench.py's hardware-in-the-loop block on the tiny workload: more GPU tier -> more doc
+    hits -> lower executed TTFT; the timed SLO bisection returns a rate within bounds."""
+    import os
+
+    from ragsim.cost_model import save_profile_csv, synthetic_profile
+
+    from paper_2404_12457_b200.timed_curves import (TimedRunner, timed_slo_throughput,
+                                                    timed_ttft_curve)
+    from paper_2404_12457_b200.workloads import WORKLOADS
+
+    w = WORKLOADS["tiny-1k"]
+    path = os.path.join("/tmp", "tiny_profile_test.csv")
+    save_profile_csv(synthetic_profile(), path)
+    runner = TimedRunner(w, 20_000, 0)
+    kw = dict(prof_path=path, dec_ms=2.0, stage_ms=1.0, pcie_gbs=50.0)
+    rows = timed_ttft_curve(runner, [1200, 20_000], n_requests=150, **kw)
+    assert rows[1]["doc_hit_rate"] > rows[0]["doc_hit_rate"]
+    assert all(r["prefills_executed"] >= 150 for r in rows)
+    slo = timed_slo_throughput(runner, 20_000, n_requests=80, iterations=2, max_rate=100.0, **kw)
+    assert 0.5 <= slo["req_per_s_at_slo"] <= 100.0 and len(slo["probes"]) >= 2
+    runner.close()

@@ -52,6 +52,10 @@ def parse():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--cache-warm-steps", type=int, default=40)
     ap.add_argument("--swap-mode", type=int, default=0)
+    ap.add_argument("--layers-per-group", type=int, default=1,
+                    help="a step's swaps are issued per group of this many layers and each "
+                         "layer's K/V write + attention waits only for its group (0: the whole "
+                         "batch before the prefill)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ttft", action="store_true")
     ap.add_argument("--no-timed", action="store_true",
@@ -174,9 +178,21 @@ def make_queries(w, batch_reqs, rows: int | None = None):
     return torch.from_numpy(q.astype(np.float32)).to(torch.bfloat16)
 
 
+def fence_step(dpool, compute, swapped: bool, layers_per_group: int):
+    """Issue the step's pending swaps and order the prefill after them.  With swaps and
+    layers_per_group > 0 they go out per layer group (swap-outs off the critical path:
+    layer l's K/V write waits only for the swap-outs' layer-l slices of the blocks it
+    reuses, simulator.py:505-507); returns the per-layer fence for HotPath.prefill."""
+    if swapped and layers_per_group > 0:
+        dpool.flush_layered(layers_per_group)
+        return lambda layer: dpool.fence_layer(layer, compute)
+    dpool.fence_into(compute)
+    return None
+
+
 def run_ours(args, dist: Dist):
     from paper_2404_12457_b200 import _lib, synth
-    from paper_2404_12457_b200.hotpath import HotPath, StepPlan, apply_events, EventLog
+    from paper_2404_12457_b200.hotpath import HotPath, StepPlan, apply_events, EventLog, has_swaps
     from paper_2404_12457_b200.pool import accounting_pool
     from paper_2404_12457_b200.retrieval import ShardedRetriever
     from paper_2404_12457_b200.workloads import pool_blocks
@@ -264,8 +280,8 @@ def run_ours(args, dist: Dist):
         if scan_events is not None:
             scan_events[-1][1].record()
         apply_events(dpool, p.events)
-        dpool.fence_into(compute)
-        device.prefill(p, qkv, q_rot, out, events=attn_events)
+        fence = fence_step(dpool, compute, has_swaps(p.events), args.layers_per_group)
+        device.prefill(p, qkv, q_rot, out, events=attn_events, layer_fence=fence)
         dpool.wait_for(compute)
         apply_events(dpool, p.commit_events)
         return ids
@@ -637,13 +653,17 @@ def run_e2e(args, dist, w, R, steps, planner, device, dpool, retr, qkv, q_rot, o
         ok &= docs == [r.doc_sequence for r in batch]
         todo = carry + list(zip(batch, docs))
         cand = todo[:R]
+        sw0 = dpool.stats()
         adm = planner.admit_batch([(r.id, d, r.prompt_tokens) for r, d in cand])
+        sw1 = dpool.stats()
+        swapped = (sw1["swap_out_calls"], sw1["swap_in_calls"]) != (sw0["swap_out_calls"],
+                                                                    sw0["swap_in_calls"])
         carry = todo[len(adm):]
         served += len(adm)
         plan = StepPlan(adm, [], [])
         device.prepare_device(plan)
-        dpool.fence_into(compute)
-        device.prefill(plan, qkv, q_rot, out)
+        fence = fence_step(dpool, compute, swapped, args.layers_per_group)
+        device.prefill(plan, qkv, q_rot, out, layer_fence=fence)
         dpool.wait_for(compute)
         last = plan.dev["last"]
         out_host[: len(adm)].copy_(out[last], non_blocking=True)

@@ -107,11 +107,14 @@ int rcb_pool_flush(rcb_pool* pool);
 int rcb_pool_fence_into(rcb_pool* pool, void* stream);
 int rcb_pool_wait_for(rcb_pool* pool, void* stream);
 int rcb_pool_sync(rcb_pool* pool);
-/* layer-pipelined swap-in (replaces the serial charge
+/* layer-pipelined swaps (replaces the serial charge
  * `transfer_ms + prefill_ms` of _admit, simulator.py:505-510, with overlap):
- * issue the pending H2D batch as groups of `layers_per_group` layers (one
- * strided DMA per block run and group, one event per group).  A pending D2H
- * batch is issued as by rcb_pool_flush. */
+ * issue the pending swap-out (D2H) and swap-in (H2D) batches as groups of
+ * `layers_per_group` layers (one strided DMA per block run and group, on the
+ * copy engines; per group the swap-outs first, then the swap-ins; one event per
+ * group).  A prefill that fences layer l with rcb_pool_fence_layer may then
+ * write layer l of blocks freed by the swap-outs and read layer l of the
+ * swapped-in nodes while later groups are still moving. */
 int rcb_pool_flush_layered(rcb_pool* pool, int32_t layers_per_group);
 /* make `stream` wait only for the layer group holding `layer` of the last
  * layered batch (full rcb_pool_fence_into when none is outstanding) */

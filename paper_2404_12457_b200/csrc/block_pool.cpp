@@ -13,7 +13,8 @@
 // Copies are batched per direction and issued in order on one copy stream
 // (SURVEY H3): a block freed by a pending swap-out can only be rewritten by
 // work that is ordered after the flush (swap-in on the same stream, or compute
-// fenced with rcb_pool_fence_into).
+// fenced with rcb_pool_fence_into, or per layer with rcb_pool_flush_layered +
+// rcb_pool_fence_layer).
 #include <algorithm>
 #include <cstring>
 #include <functional>
@@ -81,12 +82,15 @@ struct rcb_pool {
   MinHeap gpu_free, host_free;
   std::unordered_map<int64_t, Node> nodes;
   std::unordered_map<int64_t, Gen> gens;
-  int pending_dir = 0;  // 0 none, 1 gpu->host, 2 host->gpu
-  std::vector<std::pair<int32_t, int32_t>> pending;  // (gpu block, host block)
-  // blocks touched by the pending batch: a batch never names a block twice, so
-  // one launch / one DMA sequence is order-free (a host block freed and reused
-  // inside a batch would otherwise race in the zero-copy kernel)
-  std::unordered_set<int32_t> pend_gpu, pend_host;
+  // pending copies, (gpu block, host block) pairs per direction.  Within a direction a
+  // batch never names a block twice, so one launch / one DMA sequence is order-free (a
+  // host block freed and reused inside a batch would otherwise race in the zero-copy
+  // kernel).  Both directions may be pending at once: they are always issued swap-outs
+  // first (per layer group when layered), which is the order every allowed overlap needs
+  // (a swap-in writing a GPU block a pending swap-out still reads, or reading a host
+  // block a pending swap-out writes).  Any other overlap flushes first (enqueue).
+  std::vector<std::pair<int32_t, int32_t>> pend_out, pend_in;
+  std::unordered_set<int32_t> out_gpu, out_host, in_gpu, in_host;
   int64_t stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   // layer-pipelined swap-in (rcb_pool_flush_layered): one event per layer group
   // of the last layered H2D batch; invalidated by any later copy issue
@@ -143,28 +147,21 @@ int issue_runs(rcb_pool* p, const std::vector<std::pair<int32_t, int32_t>>& pr, 
   return RCB_OK;
 }
 
-int flush(rcb_pool* p) {
-  if (p->swap_mode == RCB_POOL_ACCOUNTING) {
-    const int64_t moved = static_cast<int64_t>(p->pending.size()) * p->block_bytes;
-    if (p->pending_dir == 1) p->stats[2] += moved;
-    if (p->pending_dir == 2) p->stats[3] += moved;
-    p->pending.clear();
-    p->pend_gpu.clear();
-    p->pend_host.clear();
-    p->pending_dir = 0;
-    return RCB_OK;
-  }
-  if (p->pending_dir == 0 || p->pending.empty()) {
-    p->pending_dir = 0;
-    p->pending.clear();
-    p->pend_gpu.clear();
-    p->pend_host.clear();
-    return RCB_OK;
-  }
-  const bool to_host = p->pending_dir == 1;
-  auto& pr = p->pending;
+void clear_pending(rcb_pool* p) {
+  p->pend_out.clear();
+  p->pend_in.clear();
+  p->out_gpu.clear();
+  p->out_host.clear();
+  p->in_gpu.clear();
+  p->in_host.clear();
+}
+
+bool any_pending(const rcb_pool* p) { return !p->pend_out.empty() || !p->pend_in.empty(); }
+
+// one direction's batch, whole blocks, in the pool's swap mode
+int issue_batch(rcb_pool* p, const std::vector<std::pair<int32_t, int32_t>>& pr, bool to_host) {
+  if (pr.empty()) return RCB_OK;
   int rc = RCB_OK;
-  p->layered_groups = 0;  // later copies are not covered by the per-layer events
   if (p->swap_mode == RCB_SWAP_ZEROCOPY) {
     for (size_t lo = 0; lo < pr.size() && rc == RCB_OK; lo += rcb::kPairsPerLaunch) {
       const size_t hi = std::min(pr.size(), lo + rcb::kPairsPerLaunch);
@@ -204,40 +201,59 @@ int flush(rcb_pool* p) {
     for (size_t lo = 0; lo < pr.size() && rc == RCB_OK; lo += chunk)
       rc = issue_runs(p, pr, lo, std::min(pr.size(), lo + chunk), to_host);
   }
-  const int64_t moved = static_cast<int64_t>(pr.size()) * p->block_bytes;
-  if (to_host) p->stats[2] += moved;
-  else p->stats[3] += moved;
-  p->pending.clear();
-  p->pend_gpu.clear();
-  p->pend_host.clear();
-  p->pending_dir = 0;
   return rc;
 }
 
+int flush(rcb_pool* p) {
+  const int64_t out_bytes = static_cast<int64_t>(p->pend_out.size()) * p->block_bytes;
+  const int64_t in_bytes = static_cast<int64_t>(p->pend_in.size()) * p->block_bytes;
+  int rc = RCB_OK;
+  if (p->swap_mode != RCB_POOL_ACCOUNTING && any_pending(p)) {
+    p->layered_groups = 0;  // later copies are not covered by the per-layer events
+    rc = issue_batch(p, p->pend_out, true);  // swap-outs first (see pend_out)
+    if (rc == RCB_OK) rc = issue_batch(p, p->pend_in, false);
+  }
+  p->stats[2] += out_bytes;
+  p->stats[3] += in_bytes;
+  clear_pending(p);
+  return rc;
+}
+
+// dir 1: swap-out (GPU g -> host h), 2: swap-in (host h -> GPU g)
 int enqueue(rcb_pool* p, int dir, const std::vector<int32_t>& g, const std::vector<int32_t>& h) {
-  bool conflict = p->pending_dir != 0 && p->pending_dir != dir;
-  for (size_t i = 0; i < g.size() && !conflict; ++i)
-    conflict = p->pend_gpu.count(g[i]) || p->pend_host.count(h[i]);
+  bool conflict = false;
+  for (size_t i = 0; i < g.size() && !conflict; ++i) {
+    if (dir == 1)  // must follow every pending copy that touches its blocks: flush first
+      conflict = p->out_gpu.count(g[i]) || p->out_host.count(h[i]) || p->in_gpu.count(g[i]) ||
+                 p->in_host.count(h[i]);
+    else  // after a pending swap-out on the same block is fine: swap-outs issue first
+      conflict = p->in_gpu.count(g[i]) || p->in_host.count(h[i]);
+  }
   if (conflict) {
     int rc = flush(p);
     if (rc != RCB_OK) return rc;
   }
-  p->pending_dir = dir;
+  auto& list = dir == 1 ? p->pend_out : p->pend_in;
+  auto& sg = dir == 1 ? p->out_gpu : p->in_gpu;
+  auto& sh = dir == 1 ? p->out_host : p->in_host;
   for (size_t i = 0; i < g.size(); ++i) {
-    p->pending.emplace_back(g[i], h[i]);
-    p->pend_gpu.insert(g[i]);
-    p->pend_host.insert(h[i]);
+    list.emplace_back(g[i], h[i]);
+    sg.insert(g[i]);
+    sh.insert(h[i]);
   }
   return RCB_OK;
 }
 
-// Layer-pipelined swap-in: the pending H2D batch is issued as G
-// groups of `lpg` layers.  Within a block the layer slices are contiguous
-// ([L][2][H_kv][B][d_h]), so group g of a run of consecutive (gpu, host) block
-// pairs is ONE strided DMA (cudaMemcpy2DAsync: width = lpg layer slices, pitch =
-// block_bytes, height = run length).  Event g is recorded after group g; the
-// prefill's attention for layer l waits only for its group (rcb_pool_fence_layer).
-int flush_layered_h2d(rcb_pool* p, int32_t lpg) {
+// Layer-pipelined swaps: the pending batches are issued as G groups of
+// `lpg` layers.  Within a block the layer slices are contiguous ([L][2][H_kv][B][d_h]),
+// so group g of a run of consecutive (gpu, host) block pairs is ONE strided DMA
+// (cudaMemcpy2DAsync: width = lpg layer slices, pitch = block_bytes, height = run
+// length), and the copy engines do the scatter (no SMs taken from the prefill).  Per
+// group the swap-out slices go first, then the swap-in slices (the order of pend_out);
+// event g is recorded after group g.  A prefill's layer l waits only for its group
+// (rcb_pool_fence_layer): its K/V write may then reuse blocks whose layer-l slices a
+// swap-out has already read, and its attention reads swapped-in layer-l slices.
+int flush_layered(rcb_pool* p, int32_t lpg) {
   const int32_t groups = (p->layers + lpg - 1) / lpg;
   while (static_cast<int32_t>(p->ev_layer.size()) < groups) {
     cudaEvent_t ev;
@@ -245,35 +261,45 @@ int flush_layered_h2d(rcb_pool* p, int32_t lpg) {
     if (e != cudaSuccess) return set_cuda_error(e, "pool layer event");
     p->ev_layer.push_back(ev);
   }
-  auto& pr = p->pending;
-  std::vector<std::pair<size_t, size_t>> runs;  // [i, j) with consecutive gpu and host blocks
-  for (size_t i = 0; i < pr.size();) {
-    size_t j = i + 1;
-    while (j < pr.size() && pr[j].first == pr[j - 1].first + 1 && pr[j].second == pr[j - 1].second + 1)
-      ++j;
-    runs.emplace_back(i, j);
-    i = j;
-  }
+  using Runs = std::vector<std::pair<size_t, size_t>>;  // [i, j): consecutive gpu and host blocks
+  auto runs_of = [](const std::vector<std::pair<int32_t, int32_t>>& pr) {
+    Runs runs;
+    for (size_t i = 0; i < pr.size();) {
+      size_t j = i + 1;
+      while (j < pr.size() && pr[j].first == pr[j - 1].first + 1 &&
+             pr[j].second == pr[j - 1].second + 1)
+        ++j;
+      runs.emplace_back(i, j);
+      i = j;
+    }
+    return runs;
+  };
+  const Runs runs_out = runs_of(p->pend_out), runs_in = runs_of(p->pend_in);
   const int64_t layer_bytes = p->block_bytes / p->layers;
   for (int32_t g = 0; g < groups; ++g) {
     const int32_t l0 = g * lpg, l1 = std::min(p->layers, l0 + lpg);
     const int64_t off = int64_t(l0) * layer_bytes, width = int64_t(l1 - l0) * layer_bytes;
-    for (const auto& r : runs) {
-      uint8_t* dst = p->gpu_base + int64_t(pr[r.first].first) * p->block_bytes + off;
-      const uint8_t* src = p->host_base + int64_t(pr[r.first].second) * p->block_bytes + off;
-      cudaError_t e = cudaMemcpy2DAsync(dst, p->block_bytes, src, p->block_bytes, width,
+    for (int d = 0; d < 2; ++d) {
+      const bool to_host = d == 0;
+      const auto& pr = to_host ? p->pend_out : p->pend_in;
+      for (const auto& r : to_host ? runs_out : runs_in) {
+        uint8_t* gp = p->gpu_base + int64_t(pr[r.first].first) * p->block_bytes + off;
+        uint8_t* hp = p->host_base + int64_t(pr[r.first].second) * p->block_bytes + off;
+        cudaError_t e =
+            to_host ? cudaMemcpy2DAsync(hp, p->block_bytes, gp, p->block_bytes, width,
+                                        r.second - r.first, cudaMemcpyDeviceToHost, p->stream)
+                    : cudaMemcpy2DAsync(gp, p->block_bytes, hp, p->block_bytes, width,
                                         r.second - r.first, cudaMemcpyHostToDevice, p->stream);
-      if (e != cudaSuccess) return set_cuda_error(e, "pool layered memcpy");
-      p->stats[7] += 1;
+        if (e != cudaSuccess) return set_cuda_error(e, "pool layered memcpy");
+        p->stats[7] += 1;
+      }
     }
     cudaError_t e = cudaEventRecord(p->ev_layer[g], p->stream);
     if (e != cudaSuccess) return set_cuda_error(e, "pool layer event record");
   }
-  p->stats[3] += static_cast<int64_t>(pr.size()) * p->block_bytes;
-  p->pending.clear();
-  p->pend_gpu.clear();
-  p->pend_host.clear();
-  p->pending_dir = 0;
+  p->stats[2] += static_cast<int64_t>(p->pend_out.size()) * p->block_bytes;
+  p->stats[3] += static_cast<int64_t>(p->pend_in.size()) * p->block_bytes;
+  clear_pending(p);
   p->layered_groups = groups;
   p->group_layers = lpg;
   return RCB_OK;
@@ -638,16 +664,15 @@ int rcb_pool_wait_for(rcb_pool* p, void* stream) {
 int rcb_pool_flush_layered(rcb_pool* p, int32_t layers_per_group) {
   if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
   if (layers_per_group <= 0) return set_error(RCB_ERR_ARG, "layers_per_group must be positive");
-  if (p->swap_mode == RCB_POOL_ACCOUNTING || p->pending_dir != 2 || p->pending.empty())
-    return flush(p);  // nothing to pipeline: a D2H batch (or nothing) issues as usual
-  return flush_layered_h2d(p, std::min(layers_per_group, p->layers));
+  if (p->swap_mode == RCB_POOL_ACCOUNTING || !any_pending(p)) return flush(p);
+  return flush_layered(p, std::min(layers_per_group, p->layers));
 }
 
 int rcb_pool_fence_layer(rcb_pool* p, int32_t layer, void* stream) {
   if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
   if (layer < 0 || layer >= p->layers) return set_error(RCB_ERR_ARG, "layer out of range");
   if (p->swap_mode == RCB_POOL_ACCOUNTING) return RCB_OK;
-  if (!p->pending.empty() || p->layered_groups == 0)
+  if (any_pending(p) || p->layered_groups == 0)
     return rcb_pool_fence_into(p, stream);  // no layered batch outstanding: full fence
   const int32_t g = std::min(layer / p->group_layers, p->layered_groups - 1);
   cudaError_t e = cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), p->ev_layer[g], 0);
@@ -658,8 +683,15 @@ int rcb_pool_fence_layer(rcb_pool* p, int32_t layer, void* stream) {
 int rcb_pool_drain(rcb_pool* p) {
   if (p == nullptr) return set_error(RCB_ERR_BAD_HANDLE, "null pool");
   if (p->swap_mode == RCB_POOL_ACCOUNTING) return RCB_OK;
-  if (p->pending_dir == 1) {  // a pending swap-out batch is issued and drained too
-    int rc = flush(p);
+  if (!p->pend_out.empty()) {  // a pending swap-out batch is issued and drained too; a
+    // pending swap-in batch stays pending (it is issued later on the same stream, so it
+    // still follows the swap-outs)
+    p->layered_groups = 0;
+    int rc = issue_batch(p, p->pend_out, true);
+    p->stats[2] += static_cast<int64_t>(p->pend_out.size()) * p->block_bytes;
+    p->pend_out.clear();
+    p->out_gpu.clear();
+    p->out_host.clear();
     if (rc != RCB_OK) return rc;
   }
   cudaError_t e = cudaStreamSynchronize(p->stream);

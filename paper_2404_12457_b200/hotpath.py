@@ -222,11 +222,15 @@ class HotPath:
                     "last": arr[2 * n:].long(), "flops": attention_flops(self.shape, reqs)}
 
     def prefill(self, plan: StepPlan, qkv: torch.Tensor, q_rot, out: torch.Tensor,
-                events=None, stream=None) -> None:
+                events=None, stream=None, layer_fence=None) -> None:
         """Launch KV-write + attention for every layer of the step (async).
 
         ``q_rot`` is unused (kept for callers of the pre-rotated path): Q's RoPE is
-        applied inside the attention kernel from the hot path's cos/sin table."""
+        applied inside the attention kernel from the hot path's cos/sin table.
+        ``layer_fence(layer)`` (optional) runs before a layer's K/V write: with the step's
+        swaps issued per layer group (BlockPool.flush_layered) the layer then waits only
+        for its own group, i.e. for the swap-outs that read its slices of blocks the suffix
+        now reuses and the swap-ins its attention reads."""
         s = self.shape
         d = plan.dev
         T = plan.total_q
@@ -242,6 +246,8 @@ class HotPath:
         base = self.pool.gpu_base
         rope = self.rope_table(max(1 << 15, d["attn"].max_pos))
         for layer in range(s.n_layers):
+            if layer_fence is not None:
+                layer_fence(layer)
             # K/V: RoPE + paged write; Q's RoPE is fused into the attention kernel, which
             # reads the raw query columns of the QKV rows (no rotated-Q round trip)
             kernels.kv_write_rope(None, k, v, None, d["pos"], d["slots"], base,
@@ -257,6 +263,11 @@ class HotPath:
                                    rope=rope, n_q_heads=s.n_q_heads, stream=stream)
             if events is not None:
                 events[layer][1].record()
+
+
+def has_swaps(events) -> bool:
+    """The step's pool events move bytes (a swap-out or a swap-in)."""
+    return any(ev[0] in ("node_swap_out", "node_swap_in") for ev in events)
 
 
 def attention_flops(shape: ModelShape, reqs) -> float:

@@ -63,13 +63,62 @@ def test_layered_swap_in_bytes_and_fences(n_layers, lpg):
     pool.close()
 
 
-def test_layered_flush_without_swap_in_is_plain_flush():
+@pytest.mark.parametrize("lpg", [1, 2, 6])
+def test_layered_swap_out_with_block_reuse(lpg):
+    """Swap-outs off the critical path: a swap-out and a swap-in pending in ONE batch,
+    issued per layer group (swap-outs first in every group).  A new node reuses the
+    swapped-out node's blocks and writes them layer by layer, each layer fenced on its
+    group only: the host copy still holds the old bytes, the swap-in lands intact, and
+    the new writes survive."""
+    n_layers = 6
+    geom = _geom(n_layers)
+    bb = n_layers * 2 * 2 * 16 * 64 * 2
+    lb = bb // n_layers
+    nb = 32
+    u8 = torch.zeros((nb, bb), dtype=torch.uint8, device="cuda")
+    pool = BlockPool(nb, 32, gpu_base=u8.data_ptr(), swap_mode=_lib.RCB_SWAP_STAGED, **geom)
+    pool.node_alloc_gpu(1, 70)   # blocks 0-4
+    pool.node_alloc_gpu(2, 16)   # block 5
+    pool.node_alloc_gpu(3, 40)   # blocks 6-8
+    u8.copy_(torch.randint(0, 256, u8.shape, dtype=torch.uint8, device="cuda"))
+    want1 = u8[pool.node_blocks(1)].clone()
+    want3 = u8[pool.node_blocks(3)].clone()
+    pool.node_swap_out([3])
+    pool.sync()
+    # one batch: swap-out 1, a new node 4 takes 1's freed blocks, swap-in 3
+    pool.node_swap_out([1])
+    pool.node_alloc_gpu(4, 70)
+    assert pool.node_blocks(4) == [0, 1, 2, 3, 4]
+    pool.node_swap_in([3])
+    stream = torch.cuda.current_stream()
+    pool.flush_layered(lpg)
+    new4 = torch.randint(0, 256, (5, bb), dtype=torch.uint8, device="cuda")
+    b4 = pool.node_blocks(4)
+    for layer in range(n_layers):
+        pool.fence_layer(layer, stream)  # the K/V write of this layer into reused blocks
+        u8[b4, layer * lb:(layer + 1) * lb] = new4[:, layer * lb:(layer + 1) * lb]
+    torch.cuda.synchronize()
+    st = pool.stats()
+    assert st["d2h_bytes"] == (3 + 5) * bb and st["h2d_bytes"] == 3 * bb
+    assert torch.equal(u8[pool.node_blocks(3)], want3), "swap-in bytes differ"
+    assert torch.equal(u8[b4], new4), "reused blocks lost the new writes"
+    pool.wait_for(stream)
+    pool.node_free_gpu(2)
+    pool.node_swap_in([1])  # the host copy written by the layered swap-out
+    pool.sync()
+    assert torch.equal(u8[pool.node_blocks(1)], want1), "layered swap-out bytes differ"
+    pool.close()
+
+
+def test_layered_flush_of_swap_outs_and_plain_fence():
     geom = _geom(4)
     pool = BlockPool(16, 8, swap_mode=_lib.RCB_SWAP_STAGED, **geom)
     pool.node_alloc_gpu(1, 30)
     pool.node_swap_out([1])
-    pool.flush_layered(2)  # pending D2H: issued as a normal batch
-    pool.fence_layer(3, torch.cuda.current_stream())  # no layered batch: full fence
+    pool.flush_layered(2)  # pending D2H: two layer groups
+    pool.fence_layer(3, torch.cuda.current_stream())
+    pool.flush()
+    pool.fence_layer(3, torch.cuda.current_stream())  # no layered batch outstanding: full fence
     pool.drain()
     assert pool.stats()["d2h_bytes"] == 2 * pool.block_bytes
     with pytest.raises(Exception):

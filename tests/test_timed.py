@@ -110,7 +110,7 @@ def test_timed_curves_and_slo_throughput_tiny():
     save_profile_csv(synthetic_profile(), path)
     runner = TimedRunner(w, 20_000, 0)
     kw = dict(prof_path=path, dec_ms=2.0, stage_ms=1.0, pcie_gbs=50.0)
-    rows = timed_ttft_curve(runner, [1200, 20_000], n_requests=150, **kw)
+    rows = timed_ttft_curve(runner, [5000, 20_000], n_requests=150, **kw)
     assert rows[1]["doc_hit_rate"] > rows[0]["doc_hit_rate"]
     assert all(r["prefills_executed"] >= 150 for r in rows)
     slo = timed_slo_throughput(runner, 20_000, n_requests=80, iterations=2, max_rate=100.0, **kw)

@@ -26,6 +26,8 @@
 // Key slots carry holes (node tails: a block holds `valid` <= BT tokens), so
 // each block also carries its logical start position; a slot is attended iff
 // off < valid && pos <= query_pos (causal on logical positions).
+#include <climits>
+
 #include "sm100.cuh"
 #include "rcb_internal.h"
 
@@ -50,9 +52,12 @@ constexpr int kPolyCols = RCB_POLY_COLS;
 //   softmax WG w, its tile c: [c][4w + 0] S wait start, [4w + 1] S seen, [4w + 2] P arrive
 //   MMA, step s: [s][8] P0 seen, [9] QK0 issued, [10] P1 seen, [11] QK1 issued,
 //   [12] K(s) seen full, [13] PV0 issued, [14] PV1 issued, [15] Q seen (first step of an item)
+//   producer, step s: [s][16] block ids loaded, [17] K(s) issued, [18] V(s) issued
+//   epilogue, item ii: [ii][19] O0 full seen, [20] O0 freed, [21] O1 full seen, [22] O1 freed,
+//   [23] item's O written (stores issued)
 #ifdef RCB_TRACE
 constexpr int kTraceTiles = 1024;
-constexpr int kTraceEv = 16;
+constexpr int kTraceEv = 24;
 __device__ long long g_trace[kTraceTiles * kTraceEv];
 #define TRACE(g, ev)                                                                      \
   do {                                                                                    \
@@ -280,7 +285,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             vv[b] = in ? blk_valid[it.blk_begin + sb] : 0;
             pp[b] = in ? blk_pos[it.blk_begin + sb] : 0;
           }
+#ifdef RCB_TRACE
+          if (ids[0] + vv[0] + pp[0] == INT_MIN) __trap();  // force the loads before the stamp
+#endif
+          TRACE(s, 16);
           load_kv(2 * s, 0, ids, it.kvh);
+          TRACE(s, 17);
           // per-step mask metadata: its own ring (the softmax may lag the K/V ring)
           const int ms = s & (S::kMetaSlots - 1);
           mbar_wait(&bar[kMetaFree0 + ms], ((s / S::kMetaSlots) & 1) ^ 1);
@@ -291,6 +301,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           mbar_arrive(&bar[kMetaFull0 + ms]);  // release: publishes sMeta[ms]
           load_kv(2 * s + 1, 1, ids, it.kvh);
+          TRACE(s, 18);
         }
       }
     }
@@ -490,6 +501,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const bool masked = !all_valid || max_pos > qp;
         const bool half = it.half(wg, j);  // only S columns [0, 64) were computed
+#ifdef RCB_DBG_NOSOFTMAX
+        // timing experiment only (wrong results): hand P over without computing it, so the
+        // step time is the MMA + handoff pipeline alone
+        tc_fence_before();
+        mbar_arrive(&bar[kPFull0 + wg]);
+        mbar_arrive(&bar[kPFullB0 + wg]);
+        any = true;
+        if (tr) TRACE(c, 4 * wg + 2);
+        ++c;
+        continue;
+#endif
         // Two 64-column chunks against the running max m (within 2^8 of the true row max: a
         // chunk that exceeds m + 2^8 rescales O and l).  P of chunk c (bf16 pairs) goes to S
         // columns [32c, 32c + 32) and is handed to the MMA warp per chunk, so the PV of keys
@@ -715,7 +737,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int oc[2] = {0, 0};
     // rows of query tile qt = (sum_w c_w O_w) / (sum_w c_w l_w), c_w = 2^(m_w - max m) over
     // the WGs that worked on it (one for a pair item's tile, both for a split item)
-    auto epilogue = [&](const Item& it, int qt, bool use0, bool use1, int qb) {
+    auto epilogue = [&](const Item& it, int qt, bool use0, bool use1, int qb, int ii) {
+      (void)ii;
       const int tok = (2 * it.qp + qt) * TQ + t_local;
       const bool row_valid = tok < it.q_len;
       // a full tile (every token valid) is staged in its Q buffer and TMA-stored
@@ -745,6 +768,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (part && row_valid) part_ml[static_cast<int64_t>(it.ps) * kRows + row] = make_float2(mm, l);
       if (use0) mbar_wait(&bar[kOFull0 + 0], oc[0] & 1);
       if (use1) mbar_wait(&bar[kOFull0 + 1], oc[1] & 1);
+      if (row == 0) TRACE(ii, use0 ? 19 : 21);
       tc_fence_after();
       __nv_bfloat16* orow =
           out + (static_cast<int64_t>(it.q_start + tok) * n_q_heads + it.kvh * G + h_local) * HD;
@@ -758,6 +782,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_before();
           if (use0) mbar_arrive(&bar[kOFree0 + 0]);
           if (use1) mbar_arrive(&bar[kOFree0 + 1]);
+          if (row == 0) TRACE(ii, use0 ? 20 : 22);
         }
         float o[32];
 #pragma unroll
@@ -816,6 +841,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_store_commit();
         }
       }
+      if (row == 0) TRACE(ii, 23);
       if (use0) ++oc[0];
       if (use1) ++oc[1];
     };
@@ -831,10 +857,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int ii = 0; ii < n_mine; ++ii) {
       const Item it = item_of(ii);
       if (it.split()) {
-        epilogue(it, 0, true, it.has(1), ii & 1);
+        epilogue(it, 0, true, it.has(1), ii & 1, ii);
       } else {
-        epilogue(it, 0, true, false, ii & 1);
-        if (it.has(1)) epilogue(it, 1, false, true, ii & 1);
+        epilogue(it, 0, true, false, ii & 1, ii);
+        if (it.has(1)) epilogue(it, 1, false, true, ii & 1, ii);
       }
       if (kOTma && row == 0) {  // the staged O left smem: Q(ii + 2) may land in the buffer
         tma_store_wait_read();

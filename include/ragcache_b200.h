@@ -211,7 +211,9 @@ int rcb_silu_mul(const void* gate_up_dev, void* out_dev, int32_t n_rows, int32_t
  * top-k epilogue).  Stand-in replaced: generate_stages / StagedRetrieval
  * (speculation.py:33-59,149-194) behind the StageProvider seam (simulator.py:228).
  *   corpus_dev : bf16 [n_rows][dim] (dim % 64 == 0, dim <= 1024)
- *   queries_dev: bf16 [n_queries][dim], n_queries <= 64
+ *   queries_dev: bf16 [n_queries][dim], n_queries <= 256 (more than 64: a cluster of 2 or
+ *                4 CTAs x 64 queries per corpus range, every corpus stage loaded once and
+ *                multicast to the cluster, so the corpus is read once per call)
  *   stage s (0-based) = exact top-k over rows [0, floor((s+1)*n_rows/n_stages))
  *   ids_out_dev   : int64 [n_queries][n_stages][k] (row + id_offset), score desc / id asc
  *   scores_out_dev: fp32  [n_queries][n_stages][k]

@@ -39,14 +39,15 @@ constexpr int kThreads = 512;
 constexpr int kRows = 128;
 constexpr int kKeys = 128;  // key slots per KV tile
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
-// exp2 on the FMA/ALU pipes (magic-add rounding + cubic) for kPolyCols of every 8 score
-// columns.  Measured on B200: 2 of 8 is fastest (long prefix 1106 -> 1155 TFLOP/s, mixed
-// step 859 -> 893); 4 of 8 loses (the FMA pipe then saturates).  An earlier variant that
-// rounded with floorf (FRND, not on the FMA pipe) gained nothing.
-#ifndef RCB_POLY_COLS
-#define RCB_POLY_COLS 2
+// exp2 on the FMA/ALU pipes (magic-add rounding + cubic) for kPoly16 of every 16 score
+// columns, MUFU for the rest.  Measured on B200 (2 of 16 / 4 / 6 / 8): 2 and 4 are within
+// 1% (2 is 1-2% faster on full misses), 6 loses 4%, 8 loses more (the FMA pipe saturates);
+// none at all is 4% slower.  An earlier variant that rounded with floorf (FRND, not on the
+// FMA pipe) gained nothing.
+#ifndef RCB_POLY16
+#define RCB_POLY16 2
 #endif
-constexpr int kPolyCols = RCB_POLY_COLS;
+constexpr int kPoly16 = RCB_POLY16;  // of every 16 columns (even)
 
 // Per-step handoff timestamps of CTA 0 (debug builds with -DRCB_TRACE only; tools/attn_trace.py)
 //   softmax WG w, its tile c: [c][4w + 0] S wait start, [4w + 1] S seen, [4w + 2] P arrive
@@ -577,24 +578,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             tmem_wait_st();
           }
-          // p = 2^(s*scale - m): packed FFMA2, MUFU for 8-kPolyCols of every 8 columns
+          // p = 2^(s*scale - m): packed FFMA2, MUFU for 16-kPoly16 of every 16 columns
           // and the FMA-pipe polynomial for the rest; packed FADD2 sums
           const uint64_t sc2 = f2_pack(scale_log2, scale_log2);
           const uint64_t nm2 = f2_pack(-m, -m);
           uint64_t acc0 = f2_pack(0.f, 0.f), acc1 = acc0;
 #pragma unroll
-          for (int i = 0; i < kKeys / 2; i += 8) {
-            float x[8];
+          for (int i = 0; i < kKeys / 2; i += 16) {
+            float x[16];
 #pragma unroll
-            for (int e = 0; e < 8; e += 2) f2_unpack(ffma2(f2_pack(s[i + e], s[i + e + 1]), sc2, nm2), x[e], x[e + 1]);
+            for (int e = 0; e < 16; e += 2) f2_unpack(ffma2(f2_pack(s[i + e], s[i + e + 1]), sc2, nm2), x[e], x[e + 1]);
 #pragma unroll
-            for (int e = 0; e < 8 - kPolyCols; ++e) s[i + e] = ex2_mufu(x[e]);
+            for (int e = 0; e < 16 - kPoly16; ++e) s[i + e] = ex2_mufu(x[e]);
 #pragma unroll
-            for (int e = 8 - kPolyCols; e < 8; e += 2) f2_unpack(ex2_poly2(x[e], x[e + 1]), s[i + e], s[i + e + 1]);
-            acc0 = fadd2(acc0, f2_pack(s[i + 0], s[i + 1]));
-            acc1 = fadd2(acc1, f2_pack(s[i + 2], s[i + 3]));
-            acc0 = fadd2(acc0, f2_pack(s[i + 4], s[i + 5]));
-            acc1 = fadd2(acc1, f2_pack(s[i + 6], s[i + 7]));
+            for (int e = 16 - kPoly16; e < 16; e += 2) f2_unpack(ex2_poly2(x[e], x[e + 1]), s[i + e], s[i + e + 1]);
+#pragma unroll
+            for (int e = 0; e < 16; e += 4) {
+              acc0 = fadd2(acc0, f2_pack(s[i + e], s[i + e + 1]));
+              acc1 = fadd2(acc1, f2_pack(s[i + e + 2], s[i + e + 3]));
+            }
           }
           float a0, a1, b0, b1;
           f2_unpack(acc0, a0, a1);

@@ -9,6 +9,12 @@
 // Corpus GEMM on tcgen05: A = 128 corpus rows x 64-dim atoms (TMA, SW128,
 // 5-stage ring), B = the query batch (<= 64 queries, resident in smem), D in
 // TMEM (double-buffered, 2 x NQ fp32 columns).
+// More than 64 queries (up to 256: the all-gathered queries of 4 ranks, or of 8 ranks
+// x 32): a thread-block cluster of C = 2 or 4 CTAs shares one corpus range; CTA r holds
+// queries [64r, 64r + 64) and every A stage is loaded ONCE and multicast to the C CTAs'
+// shared memory (cp.async.bulk.tensor .multicast::cluster, issuers alternating per
+// stage), each MMA commit arrives on the stage's empty barrier in all C CTAs.  The corpus
+// is then read from HBM once per step however many queries the ranks gathered.
 // Work split: every CTA scans a CONTIGUOUS range of 32-row "quads" (balanced to
 // one quad across the grid: 100K rows over 148 SMs is 21-22 quads per CTA,
 // where whole 128-row tiles would be 5 or 6); a tile is up to 4 quads of one
@@ -124,13 +130,11 @@ __device__ __forceinline__ void tmem_ld_row(uint32_t taddr, float (&v)[NQ]) {
   }
 }
 
-// The CTA's contiguous quad range [q_lo, q_hi) and the CTA owning a quad.
-__device__ __forceinline__ void cta_quads(int n_quads, int cta, int& q_lo, int& q_hi) {
-  q_lo = (int)(((long long)n_quads * cta) / gridDim.x);
-  q_hi = (int)(((long long)n_quads * (cta + 1)) / gridDim.x);
-}
-__device__ __forceinline__ int quad_owner(int qd, int n_quads) {
-  return (int)((((long long)qd + 1) * gridDim.x + n_quads - 1) / n_quads) - 1;
+// The unit's contiguous quad range [q_lo, q_hi).
+// (a scan unit is one CTA, or one cluster sharing a range through multicast)
+__device__ __forceinline__ void cta_quads(int n_quads, int unit, int n_units, int& q_lo, int& q_hi) {
+  q_lo = (int)(((long long)n_quads * unit) / n_units);
+  q_hi = (int)(((long long)n_quads * (unit + 1)) / n_units);
 }
 
 // Tile walk over a quad range: a tile is <= 4 quads of one segment.
@@ -158,7 +162,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     topk_scan_kernel(const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_c32,
                      const __grid_constant__ CUtensorMap tm_q, int atoms, int n_quads,
                      const __grid_constant__ SegInfo seg, int k, float* __restrict__ part_score,
-                     int* __restrict__ part_id, float* __restrict__ scores_out, int n_queries) {
+                     int* __restrict__ part_id, float* __restrict__ scores_out, int n_queries,
+                     int csize) {
   using Lay = Layout<NQ>;
   constexpr int kParts = Lay::kParts;
   // the merge kernel (programmatic stream serialization) may launch now; it
@@ -180,11 +185,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   constexpr uint32_t kTmemCols = (2 * NQ <= 32) ? 32 : (2 * NQ <= 64 ? 64 : 128);
+  // cluster of csize CTAs: rank r holds queries [NQ r, NQ r + NQ), all scan the unit's rows
+  const int rank = csize > 1 ? (int)cluster_ctarank() : 0;
+  const int unit = blockIdx.x / csize, n_units = gridDim.x / csize;
+  const uint16_t mc_mask = (uint16_t)((1u << csize) - 1u);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], csize);  // every CTA of the cluster releases a multicast stage
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -196,11 +205,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 5) tmem_alloc<kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
+  if (csize > 1) cluster_sync();  // peers' barriers are initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   int q_lo, q_hi;
-  cta_quads(n_quads, blockIdx.x, q_lo, q_hi);
+  cta_quads(n_quads, unit, n_units, q_lo, q_hi);
 
   if (warp == 4) {
     if (elect_one()) {
@@ -208,7 +218,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_prefetch(&tm_c32);
       tma_prefetch(&tm_q);
       mbar_arrive_expect_tx(q_full, atoms * Lay::kAtomQ);
-      for (int a = 0; a < atoms; ++a) tma_load_2d(sQ + a * Lay::kAtomQ, &tm_q, q_full, a * 64, 0);
+      for (int a = 0; a < atoms; ++a)
+        tma_load_2d(sQ + a * Lay::kAtomQ, &tm_q, q_full, a * 64, rank * NQ);
       int it = 0;
       TileWalk tw{q_lo, q_hi, 0};
       int sg, nq4;
@@ -218,16 +229,30 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int st = it % kStages;
           mbar_wait(&empty[st], ((it / kStages) & 1) ^ 1);
           uint8_t* dst = sA + st * Lay::kA;
+          // every CTA expects the stage's bytes; one of them (alternating) loads and
+          // multicasts it to all, once every CTA's MMA released the stage (empty[st])
+          const bool issue = csize == 1 || it % csize == rank;
           if (nq4 == 4) {
             mbar_arrive_expect_tx(&full[st], Lay::kA);
-            tma_load_2d(dst, &tm_c, &full[st], a * 64, (int)r0);
+            if (csize == 1) tma_load_2d(dst, &tm_c, &full[st], a * 64, (int)r0);
+            else if (issue) tma_load_2d_mc(dst, &tm_c, &full[st], a * 64, (int)r0, mc_mask);
           } else {
             mbar_arrive_expect_tx(&full[st], nq4 * kQuad * 128);
-            for (int j = 0; j < nq4; ++j)
-              tma_load_2d(dst + j * kQuad * 128, &tm_c32, &full[st], a * 64, (int)r0 + j * kQuad);
+            for (int j = 0; j < nq4; ++j) {
+              if (csize == 1)
+                tma_load_2d(dst + j * kQuad * 128, &tm_c32, &full[st], a * 64, (int)r0 + j * kQuad);
+              else if (issue)
+                tma_load_2d_mc(dst + j * kQuad * 128, &tm_c32, &full[st], a * 64,
+                               (int)r0 + j * kQuad, mc_mask);
+            }
           }
         }
       }
+      // producer tail (clusters): every CTA's release of every stage has arrived here
+      // before this CTA may exit, so no peer's multicast commit targets a finished CTA
+      if (csize > 1)
+        for (int t = 0; t < kStages; ++t, ++it)
+          mbar_wait(&empty[it % kStages], ((it / kStages) & 1) ^ 1);
     }
   } else if (warp == 5) {
     if (elect_one()) {
@@ -254,7 +279,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t db = sw128_desc(q_base + a * Lay::kAtomQ + kk * 32, 16, 1024);
             umma_bf16_ss(tmem + buf * NQ, da, db, idesc, (a > 0 || kk > 0) ? 1u : 0u);
           }
-          umma_commit(&empty[st]);
+          if (csize > 1) umma_commit_mc(&empty[st], mc_mask);
+          else umma_commit(&empty[st]);
         }
         umma_commit(&acc_full[buf]);
       }
@@ -285,9 +311,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int p = 1; p < kParts; ++p)
 #pragma unroll
           for (int i = 0; i < KL; ++i) list_push<KL>(ls, li_, ms[(p * NQ + q) * KL + i], mi[(p * NQ + q) * KL + i]);
-        // workspace [segment][query][CTA][k]: the merging warp of (segment, query)
-        // reads the covering CTAs' candidates contiguously
-        const long long base = (((long long)sg * NQ + q) * gridDim.x + blockIdx.x) * k;
+        // workspace [segment][query][unit][k]: the merging warp of (segment, query)
+        // reads the covering units' candidates contiguously
+        const long long base = (((long long)sg * NQ * csize + rank * NQ + q) * n_units + unit) * k;
 #pragma unroll
         for (int i = 0; i < KL; ++i)
           if (i < k) {
@@ -317,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (scores_out != nullptr && r0 + tid < r1) {
 #pragma unroll
         for (int c = 0; c < NQ; ++c)
-          if (c < n_queries) scores_out[(r0 + tid) * n_queries + c] = v[c];
+          if (rank * NQ + c < n_queries) scores_out[(r0 + tid) * n_queries + rank * NQ + c] = v[c];
       }
       named_bar_sync(1, 128);  // previous tile's readers are done with sT
 #pragma unroll
@@ -342,6 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
   }
+  if (csize > 1) cluster_sync();  // no CTA leaves while a peer may still multicast into it
 }
 
 // grid = n_queries, block = 32 * n_seg; warp s reduces the candidates of the
@@ -466,7 +493,11 @@ int num_sms() {
   return sms;
 }
 
+constexpr int kMaxQueries = 256;
+// queries per CTA (padded) and CTAs per cluster: <= 64 queries run on one CTA per range,
+// more as a cluster of 2 or 4 CTAs x 64 queries sharing each multicast corpus stage
 int nq_pad(int n) { return n <= 16 ? 16 : (n <= 32 ? 32 : 64); }
+int cluster_for(int n) { return n <= 64 ? 1 : (n <= 128 ? 2 : 4); }
 
 void make_segments(int64_t n_rows, int n_stages, SegInfo& seg, int& n_quads) {
   seg.n_seg = n_stages;
@@ -484,23 +515,25 @@ void make_segments(int64_t n_rows, int n_stages, SegInfo& seg, int& n_quads) {
   n_quads = q;
 }
 
-int grid_for(int n_quads) {
-  const int g = num_sms();
+// scan units (a CTA, or a cluster of csize CTAs) over the corpus ranges
+int units_for(int n_quads, int csize) {
+  const int g = num_sms() / csize;
   return n_quads < g ? (n_quads > 0 ? n_quads : 1) : g;
 }
 
-// workspace: partial lists [n_seg][NQ][grid][k] (score f32, then id i32)
+// workspace: partial lists [n_seg][NQ * csize][units][k] (score f32, then id i32)
 int64_t part_entries(int64_t n_rows, int n_queries, int k, int n_stages) {
   SegInfo seg;
   int n_quads;
   make_segments(n_rows, n_stages, seg, n_quads);
-  return int64_t(n_stages) * nq_pad(n_queries) * grid_for(n_quads) * (k < 1 ? 1 : k);
+  const int cs = cluster_for(n_queries);
+  return int64_t(n_stages) * nq_pad(n_queries) * cs * units_for(n_quads, cs) * (k < 1 ? 1 : k);
 }
 
 template <int NQ, int KL>
 int run_scan_kl(const CUtensorMap& tc, const CUtensorMap& tc32, const CUtensorMap& tq, int atoms,
                 int n_quads, const SegInfo& seg, int k, float* part_score, int* part_id,
-                float* scores_out, int n_queries, int grid,
+                float* scores_out, int n_queries, int units, int csize,
                 cudaStream_t stream) {
   const uint32_t smem = Layout<NQ>::total(atoms);
   auto kern = topk_scan_kernel<NQ, KL>;
@@ -510,9 +543,21 @@ int run_scan_kl(const CUtensorMap& tc, const CUtensorMap& tc32, const CUtensorMa
     if (e != cudaSuccess) return set_cuda_error(e, "retrieval smem attr");
     smem_set = smem;
   }
-  kern<<<grid, kThreads, smem, stream>>>(tc, tc32, tq, atoms, n_quads, seg, k, part_score, part_id,
-                                         scores_out, n_queries);
-  cudaError_t e = cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(units * csize);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = csize;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = csize > 1 ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tc, tc32, tq, atoms, n_quads, seg, k, part_score,
+                                     part_id, scores_out, n_queries, csize);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "retrieval scan launch");
   return RCB_OK;
 }
@@ -520,7 +565,7 @@ int run_scan_kl(const CUtensorMap& tc, const CUtensorMap& tc32, const CUtensorMa
 template <int NQ>
 int run_scan(const void* corpus, int64_t n_rows, int dim, const void* queries, int n_queries,
              int n_stages, int k, float* part_score, int* part_id, float* scores_out,
-             int grid, cudaStream_t stream) {
+             int units, int csize, cudaStream_t stream) {
   SegInfo seg;
   int n_quads;
   make_segments(n_rows, n_stages, seg, n_quads);
@@ -544,26 +589,26 @@ int run_scan(const void* corpus, int64_t n_rows, int dim, const void* queries, i
   }
   const int atoms = dim / 64;
   if (k <= 2)
-    return run_scan_kl<NQ, 2>(tc, tc32, tq, atoms, n_quads, seg, k, part_score, part_id, scores_out, n_queries, grid, stream);
+    return run_scan_kl<NQ, 2>(tc, tc32, tq, atoms, n_quads, seg, k, part_score, part_id, scores_out, n_queries, units, csize, stream);
   if (k <= 4)
-    return run_scan_kl<NQ, 4>(tc, tc32, tq, atoms, n_quads, seg, k, part_score, part_id, scores_out, n_queries, grid, stream);
-  return run_scan_kl<NQ, 8>(tc, tc32, tq, atoms, n_quads, seg, k, part_score, part_id, scores_out, n_queries, grid, stream);
+    return run_scan_kl<NQ, 4>(tc, tc32, tq, atoms, n_quads, seg, k, part_score, part_id, scores_out, n_queries, units, csize, stream);
+  return run_scan_kl<NQ, 8>(tc, tc32, tq, atoms, n_quads, seg, k, part_score, part_id, scores_out, n_queries, units, csize, stream);
 }
 
 int scan(const void* corpus, int64_t n_rows, int dim, const void* queries, int n_queries,
          int n_stages, int k, float* part_score, int* part_id, float* scores_out,
-         int grid, cudaStream_t stream) {
+         int units, int csize, cudaStream_t stream) {
   switch (nq_pad(n_queries)) {
-    case 16: return run_scan<16>(corpus, n_rows, dim, queries, n_queries, n_stages, k, part_score, part_id, scores_out, grid, stream);
-    case 32: return run_scan<32>(corpus, n_rows, dim, queries, n_queries, n_stages, k, part_score, part_id, scores_out, grid, stream);
-    default: return run_scan<64>(corpus, n_rows, dim, queries, n_queries, n_stages, k, part_score, part_id, scores_out, grid, stream);
+    case 16: return run_scan<16>(corpus, n_rows, dim, queries, n_queries, n_stages, k, part_score, part_id, scores_out, units, csize, stream);
+    case 32: return run_scan<32>(corpus, n_rows, dim, queries, n_queries, n_stages, k, part_score, part_id, scores_out, units, csize, stream);
+    default: return run_scan<64>(corpus, n_rows, dim, queries, n_queries, n_stages, k, part_score, part_id, scores_out, units, csize, stream);
   }
 }
 
 int check_args(int64_t n_rows, int dim, int n_queries, int n_stages) {
   if (n_rows <= 0 || n_rows >= INT_MAX) return set_error(RCB_ERR_ARG, "n_rows out of range");
   if (dim <= 0 || dim % 64 != 0 || dim / 64 > kMaxAtoms) return set_error(RCB_ERR_ARG, "dim must be a multiple of 64, <= 1024");
-  if (n_queries <= 0 || n_queries > 64) return set_error(RCB_ERR_ARG, "1 <= n_queries <= 64");
+  if (n_queries <= 0 || n_queries > kMaxQueries) return set_error(RCB_ERR_ARG, "1 <= n_queries <= 256");
   if (n_stages <= 0 || n_stages > kMaxSeg) return set_error(RCB_ERR_ARG, "1 <= n_stages <= 8");
   return RCB_OK;
 }
@@ -592,12 +637,13 @@ extern "C" int rcb_retrieval_topk(const void* corpus_dev, int64_t n_rows, int32_
   ret::SegInfo seg;
   int n_quads;
   ret::make_segments(n_rows, n_stages, seg, n_quads);
-  const int grid = ret::grid_for(n_quads);
+  const int csize = ret::cluster_for(n_queries);
+  const int units = ret::units_for(n_quads, csize);
   float* ps = static_cast<float*>(workspace_dev);
   int* pi = reinterpret_cast<int*>(ps + entries);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   rc = ret::scan(corpus_dev, n_rows, dim, queries_dev, n_queries, n_stages, k, ps, pi, nullptr,
-                 grid, st);
+                 units, csize, st);
   if (rc != RCB_OK) return rc;
   // programmatic dependent launch: the merge's launch overlaps the scan's tail
   cudaLaunchConfig_t cfg = {};
@@ -610,8 +656,8 @@ extern "C" int rcb_retrieval_topk(const void* corpus_dev, int64_t n_rows, int32_
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, ret::topk_merge_kernel, static_cast<const float*>(ps),
-                                     static_cast<const int*>(pi), grid, n_quads,
-                                     ret::nq_pad(n_queries), seg, k,
+                                     static_cast<const int*>(pi), units, n_quads,
+                                     ret::nq_pad(n_queries) * csize, seg, k,
                                      static_cast<long long>(id_offset),
                                      reinterpret_cast<long long*>(ids_out_dev), scores_out_dev);
   if (e == cudaSuccess) e = cudaGetLastError();
@@ -628,7 +674,8 @@ extern "C" int rcb_retrieval_scores(const void* corpus_dev, int64_t n_rows, int3
   ret::SegInfo seg;
   int n_quads;
   ret::make_segments(n_rows, 1, seg, n_quads);
-  const int grid = ret::grid_for(n_quads);
+  const int csize = ret::cluster_for(n_queries);
+  const int units = ret::units_for(n_quads, csize);
   void* buf = nullptr;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaMallocAsync(&buf, entries * 8, st);
@@ -636,7 +683,7 @@ extern "C" int rcb_retrieval_scores(const void* corpus_dev, int64_t n_rows, int3
   float* ps = static_cast<float*>(buf);
   int* pi = reinterpret_cast<int*>(ps + entries);
   rc = ret::scan(corpus_dev, n_rows, dim, queries_dev, n_queries, 1, 1, ps, pi, scores_out_dev,
-                 grid, st);
+                 units, csize, st);
   cudaFreeAsync(buf, st);
   return rc;
 }

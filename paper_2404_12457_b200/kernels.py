@@ -280,7 +280,8 @@ def silu_mul(gate_up: torch.Tensor, stream=None) -> torch.Tensor:
     return out
 
 
-MAX_SCAN_QUERIES = 64  # queries per rcb_retrieval_topk call (rcb_retrieval.cu check_args)
+MAX_SCAN_QUERIES = 256  # queries per rcb_retrieval_topk call (retrieval.cu kMaxQueries; > 64 runs as
+#                         a 2- or 4-CTA cluster sharing each multicast corpus stage)
 
 
 class RetrievalWorkspace:

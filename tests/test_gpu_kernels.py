@@ -72,6 +72,10 @@ def test_block_copy_pinned_host_roundtrip():
     # quad-balanced ranges / merge edge cases: empty stage segments (rows < stages), fewer rows than k,
     # ~one 32-row quad per CTA, many tiles per CTA with ragged quads
     (5, 3, 2, 8), (33, 3, 4, 8), (4741, 7, 3, 3), (150001, 64, 2, 4), (262144, 33, 1, 5),
+    # > 64 queries: 2- and 4-CTA clusters sharing multicast corpus stages (ragged last CTA,
+    # fewer rows than one quad per cluster, full 256)
+    (20011, 65, 5, 4), (100003, 128, 2, 4), (3000, 130, 8, 1), (7, 200, 2, 3),
+    (150001, 256, 2, 4),
 ])
 def test_retrieval_scores_and_topk_exact(n_rows, b, k, stages):
     corpus = synth.corpus_int(n_rows, seed=n_rows)
@@ -107,12 +111,14 @@ def test_retrieval_workspace_reuse():
         assert np.array_equal(sc.cpu().numpy().astype(np.float64), o_sc)
 
 
-def test_retrieval_ties_break_by_id():
-    # heavy ties: rows drawn from a tiny alphabet, many duplicates
+@pytest.mark.parametrize("b", [20, 150])
+def test_retrieval_ties_break_by_id(b):
+    # heavy ties: rows drawn from a tiny alphabet, many duplicates (150 queries: a 4-CTA
+    # cluster, ties must still break by id across the multicast CTAs' partial lists)
     rng = np.random.default_rng(3)
     base = rng.integers(-1, 2, size=(7, synth.EMB_DIM)).astype(np.int8)
     corpus = base[rng.integers(0, 7, size=5000)]
-    q = rng.integers(-3, 4, size=(20, synth.EMB_DIM)).astype(np.float64)
+    q = rng.integers(-3, 4, size=(b, synth.EMB_DIM)).astype(np.float64)
     c_dev = torch.from_numpy(corpus.astype(np.float32)).to("cuda", torch.bfloat16)
     q_dev = torch.from_numpy(q.astype(np.float32)).to("cuda", torch.bfloat16)
     ids, sc = kernels.retrieval_topk(c_dev, q_dev, 8, 4)

@@ -35,7 +35,7 @@ def test_device_corpus_is_bit_identical_to_host_generator():
         assert np.array_equal(dev, host)
 
 
-@pytest.mark.parametrize("k,stages,n_req", [(2, 4, 64), (5, 4, 48), (2, 8, 33)])
+@pytest.mark.parametrize("k,stages,n_req", [(2, 4, 64), (5, 4, 48), (2, 8, 33), (2, 4, 256)])
 def test_real_corpus_100k_margin_exact(k, stages, n_req):
     n_rows = 100_000
     corpus = synth.corpus_f32(n_rows, seed=0)

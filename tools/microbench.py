@@ -139,7 +139,21 @@ def bench_retrieval():
     hbm, _ = peaks()
     n = 100_000
     corpus = synth.corpus_device(n, seed=0)
-    for b in (64, 32, 16, 1):
+    # shard-scale comparison: a 10M corpus over 8 ranks is a 1.25M-row shard per rank, and the
+    # ranks' all-gathered queries come to 8 x 32 = 256 per step: one pass of 256 (a 4-CTA
+    # cluster per range, corpus stages multicast) against four passes of 64
+    shard = synth.corpus_device(1_250_000, seed=0)
+    qb = torch.randint(-100, 100, (256, synth.EMB_DIM), device="cuda").to(torch.bfloat16)
+    ws256 = kernels.RetrievalWorkspace(shard.shape[0], 256, 2, 4)
+    ws64 = kernels.RetrievalWorkspace(shard.shape[0], 64, 2, 4)
+    one, _ = timed(lambda: kernels.retrieval_topk(shard, qb, 2, 4, workspace=ws256))
+    four, _ = timed(lambda: [kernels.retrieval_topk(shard, qb[i:i + 64], 2, 4, workspace=ws64)
+                             for i in range(0, 256, 64)])
+    sb = shard.shape[0] * synth.EMB_DIM * 2
+    emit(kind="retrieval_shard_256q", rows=shard.shape[0], queries=256, one_pass_ms=one,
+         four_passes_of_64_ms=four, one_pass_gbs=sb / one / 1e6, one_pass_frac_hbm=sb / one / 1e6 / hbm)
+    del shard, ws256, ws64
+    for b in (256, 128, 64, 32, 16, 1):
         q = torch.randint(-100, 100, (b, synth.EMB_DIM), device="cuda").to(torch.bfloat16)
         ws = kernels.RetrievalWorkspace(n, b, 2, 4)
         ids = torch.empty((b, 4, 2), dtype=torch.int64, device="cuda")

@@ -533,7 +533,7 @@ int64_t part_entries(int64_t n_rows, int n_queries, int k, int n_stages) {
 template <int NQ, int KL>
 int run_scan_kl(const CUtensorMap& tc, const CUtensorMap& tc32, const CUtensorMap& tq, int atoms,
                 int n_quads, const SegInfo& seg, int k, float* part_score, int* part_id,
-                float* scores_out, int n_queries, int units, int csize,
+                float* scores_out, int n_queries, int& units, int csize,
                 cudaStream_t stream) {
   const uint32_t smem = Layout<NQ>::total(atoms);
   auto kern = topk_scan_kernel<NQ, KL>;
@@ -555,6 +555,18 @@ int run_scan_kl(const CUtensorMap& tc, const CUtensorMap& tc32, const CUtensorMa
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = csize > 1 ? 1 : 0;
+  if (csize > 1) {
+    // clusters live inside one GPC: at most this many are co-resident; a second wave would
+    // double the scan, so the ranges are cut for the resident clusters only
+    static int max_clusters[5] = {0, 0, 0, 0, 0};  // per instantiation and cluster size
+    if (max_clusters[csize] == 0) {
+      int n = 0;
+      cudaError_t e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+      max_clusters[csize] = (e == cudaSuccess && n > 0) ? n : num_sms() / csize;
+    }
+    if (units > max_clusters[csize]) units = max_clusters[csize];
+    cfg.gridDim = dim3(units * csize);
+  }
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tc, tc32, tq, atoms, n_quads, seg, k, part_score,
                                      part_id, scores_out, n_queries, csize);
   if (e == cudaSuccess) e = cudaGetLastError();
@@ -565,7 +577,7 @@ int run_scan_kl(const CUtensorMap& tc, const CUtensorMap& tc32, const CUtensorMa
 template <int NQ>
 int run_scan(const void* corpus, int64_t n_rows, int dim, const void* queries, int n_queries,
              int n_stages, int k, float* part_score, int* part_id, float* scores_out,
-             int units, int csize, cudaStream_t stream) {
+             int& units, int csize, cudaStream_t stream) {
   SegInfo seg;
   int n_quads;
   make_segments(n_rows, n_stages, seg, n_quads);
@@ -597,7 +609,7 @@ int run_scan(const void* corpus, int64_t n_rows, int dim, const void* queries, i
 
 int scan(const void* corpus, int64_t n_rows, int dim, const void* queries, int n_queries,
          int n_stages, int k, float* part_score, int* part_id, float* scores_out,
-         int units, int csize, cudaStream_t stream) {
+         int& units, int csize, cudaStream_t stream) {
   switch (nq_pad(n_queries)) {
     case 16: return run_scan<16>(corpus, n_rows, dim, queries, n_queries, n_stages, k, part_score, part_id, scores_out, units, csize, stream);
     case 32: return run_scan<32>(corpus, n_rows, dim, queries, n_queries, n_stages, k, part_score, part_id, scores_out, units, csize, stream);
@@ -638,7 +650,7 @@ extern "C" int rcb_retrieval_topk(const void* corpus_dev, int64_t n_rows, int32_
   int n_quads;
   ret::make_segments(n_rows, n_stages, seg, n_quads);
   const int csize = ret::cluster_for(n_queries);
-  const int units = ret::units_for(n_quads, csize);
+  int units = ret::units_for(n_quads, csize);  // the scan may launch fewer (resident clusters)
   float* ps = static_cast<float*>(workspace_dev);
   int* pi = reinterpret_cast<int*>(ps + entries);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -675,7 +687,7 @@ extern "C" int rcb_retrieval_scores(const void* corpus_dev, int64_t n_rows, int3
   int n_quads;
   ret::make_segments(n_rows, 1, seg, n_quads);
   const int csize = ret::cluster_for(n_queries);
-  const int units = ret::units_for(n_quads, csize);
+  int units = ret::units_for(n_quads, csize);
   void* buf = nullptr;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaMallocAsync(&buf, entries * 8, st);

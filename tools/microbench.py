@@ -146,13 +146,17 @@ def bench_retrieval():
     qb = torch.randint(-100, 100, (256, synth.EMB_DIM), device="cuda").to(torch.bfloat16)
     ws256 = kernels.RetrievalWorkspace(shard.shape[0], 256, 2, 4)
     ws64 = kernels.RetrievalWorkspace(shard.shape[0], 64, 2, 4)
+    ws128 = kernels.RetrievalWorkspace(shard.shape[0], 128, 2, 4)
     one, _ = timed(lambda: kernels.retrieval_topk(shard, qb, 2, 4, workspace=ws256))
+    two, _ = timed(lambda: [kernels.retrieval_topk(shard, qb[i:i + 128], 2, 4, workspace=ws128)
+                            for i in range(0, 256, 128)])
     four, _ = timed(lambda: [kernels.retrieval_topk(shard, qb[i:i + 64], 2, 4, workspace=ws64)
                              for i in range(0, 256, 64)])
     sb = shard.shape[0] * synth.EMB_DIM * 2
     emit(kind="retrieval_shard_256q", rows=shard.shape[0], queries=256, one_pass_ms=one,
-         four_passes_of_64_ms=four, one_pass_gbs=sb / one / 1e6, one_pass_frac_hbm=sb / one / 1e6 / hbm)
-    del shard, ws256, ws64
+         two_passes_of_128_ms=two, four_passes_of_64_ms=four, one_pass_gbs=sb / one / 1e6,
+         one_pass_frac_hbm=sb / one / 1e6 / hbm)
+    del shard, ws256, ws64, ws128
     for b in (256, 128, 64, 32, 16, 1):
         q = torch.randint(-100, 100, (b, synth.EMB_DIM), device="cuda").to(torch.bfloat16)
         ws = kernels.RetrievalWorkspace(n, b, 2, 4)

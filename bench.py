@@ -125,7 +125,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(loaded), "source": "nvml, 5 ms"}
 
 
-NCU_TAG = "r1g"  # profiles/<tag>_ncu_summary.json: captures of the current kernels
+NCU_TAG = "r2a"  # profiles/<tag>_ncu_summary.json: captures of the current kernels
 
 
 def ncu_traffic(capture: str):
@@ -645,8 +645,12 @@ def run_e2e(args, dist, w, R, steps, planner, device, dpool, retr, qkv, q_rot, o
     # prefill runs, so the host's admissions/commits overlap device work
     launch_retrieval(0)
     carry = []  # (request, retrieved docs) deferred by a full GPU tier: served first next step
+    hs = dict.fromkeys(("wait_ids", "admit", "prepare", "launch", "commit"), 0.0)
+    pc = time.perf_counter
     for i, batch in enumerate(extra):
+        ta = pc()
         ids_ready[i & 1].synchronize()
+        hs["wait_ids"] += pc() - ta
         if i + 1 < len(extra):
             launch_retrieval(i + 1)
         docs = [tuple(int(x) for x in row) for row in ids_host[i & 1][: len(batch), -1].numpy()]
@@ -654,21 +658,30 @@ def run_e2e(args, dist, w, R, steps, planner, device, dpool, retr, qkv, q_rot, o
         todo = carry + list(zip(batch, docs))
         cand = todo[:R]
         sw0 = dpool.stats()
+        ta = pc()
         adm = planner.admit_batch([(r.id, d, r.prompt_tokens) for r, d in cand])
+        tb = pc()
+        hs["admit"] += tb - ta
         sw1 = dpool.stats()
         swapped = (sw1["swap_out_calls"], sw1["swap_in_calls"]) != (sw0["swap_out_calls"],
                                                                     sw0["swap_in_calls"])
         carry = todo[len(adm):]
         served += len(adm)
         plan = StepPlan(adm, [], [])
+        ta = pc()
         device.prepare_device(plan)
+        tb = pc()
+        hs["prepare"] += tb - ta
         fence = fence_step(dpool, compute, swapped, args.layers_per_group)
         device.prefill(plan, qkv, q_rot, out, layer_fence=fence)
         dpool.wait_for(compute)
         last = plan.dev["last"]
         out_host[: len(adm)].copy_(out[last], non_blocking=True)
+        ta = pc()
+        hs["launch"] += ta - tb
         for a in adm:
             planner.commit(a)
+        hs["commit"] += pc() - ta
         hits += sum(len(a.matched) for a in adm)
         docs_total += sum(len(a.docs) for a in adm)
         h2d += host_q[i].numel() * 2 + plan.dev["attn"]._buf.numel() * 4 + \
@@ -683,6 +696,7 @@ def run_e2e(args, dist, w, R, steps, planner, device, dpool, retr, qkv, q_rot, o
             "doc_hit_rate": round(hits / max(1, docs_total), 4),
             "h2d_bytes_per_step": int(h2d // K), "d2h_bytes_per_step": int(d2h // K),
             "ms_per_step": round(el * 1e3 / K, 3), "retrieval_matches_ground_truth": bool(ok),
+            "host_ms_per_step": {k: round(v * 1e3 / K, 3) for k, v in hs.items()},
             "includes": "host ragsim decisions + pool events + planning + H2D/D2H + kernels; "
                         "retrieval on a side stream, host decisions overlap the previous "
                         "step's prefill"}

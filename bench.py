@@ -126,6 +126,7 @@ class ClockSampler:
 
 
 NCU_TAG = "r2a"  # profiles/<tag>_ncu_summary.json: captures of the current kernels
+E2E_WARM = 2  # untimed live steps before the e2e timing
 
 
 def ncu_traffic(capture: str):
@@ -156,7 +157,7 @@ def build_workload(args, dist: Dist):
     w = WORKLOADS[args.workload]
     R = args.batch or w.batch
     # cache warm-up + warmup + timed (planned) steps, then K fresh steps for e2e
-    n_steps = args.cache_warm_steps + args.warmup + 2 * args.steps
+    n_steps = args.cache_warm_steps + args.warmup + 2 * args.steps + E2E_WARM
     n_req = n_steps * R * dist.world
     trace, sizes = make_stream(w, n_req, rate=1.0)
     mine = route(trace, dist.rank, dist.world)  # DP routing: id mod G
@@ -614,7 +615,9 @@ def run_e2e(args, dist, w, R, steps, planner, device, dpool, retr, qkv, q_rot, o
     planner.tree.pool = dpool
     K = args.steps
     n_done = args.cache_warm_steps + args.warmup + args.steps
-    extra = steps[n_done:n_done + K]  # fresh requests (never planned)
+    # fresh requests (never planned): E2E_WARM untimed live steps first (first-touch costs of
+    # the live path: pinned staging, allocator growth), then the K timed ones
+    extra = steps[n_done:n_done + E2E_WARM + K]
     host_q = [make_queries(w, b, R).pin_memory() for b in extra]
     q_dev = [torch.empty((R, host_q[0].shape[1]), dtype=torch.bfloat16, device="cuda")
              for _ in range(2)]
@@ -638,9 +641,6 @@ def run_e2e(args, dist, w, R, steps, planner, device, dpool, retr, qkv, q_rot, o
             ids_host[b].copy_(ids, non_blocking=True)
             ids_ready[b].record(rstream)
 
-    dist.barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
     # software pipeline: step i+1's retrieval runs on its own stream while step i's
     # prefill runs, so the host's admissions/commits overlap device work
     launch_retrieval(0)
@@ -648,6 +648,13 @@ def run_e2e(args, dist, w, R, steps, planner, device, dpool, retr, qkv, q_rot, o
     hs = dict.fromkeys(("wait_ids", "admit", "prepare", "launch", "commit"), 0.0)
     pc = time.perf_counter
     for i, batch in enumerate(extra):
+        if i == E2E_WARM:
+            dpool.sync()
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            h2d = d2h = hits = docs_total = served = 0
+            hs = dict.fromkeys(hs, 0.0)
         ta = pc()
         ids_ready[i & 1].synchronize()
         hs["wait_ids"] += pc() - ta

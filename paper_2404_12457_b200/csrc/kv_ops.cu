@@ -3,9 +3,10 @@
 // (1) block gather/scatter: the data path behind the knowledge tree's tier
 //     transitions (swap-out tree.py:460-473, swap-in tree.py:296-318) which the
 //     reference only prices with transfer_time (cost_model.py:120-124).  One
-//     kernel serves HBM->HBM (staging gather/scatter, compaction) and
-//     HBM<->mapped pinned host (zero-copy swap): 16-byte vector accesses, 8
-//     loads in flight per thread, grid-stride over (pair, 32 KB chunk) units.
+//     HBM->HBM copies (staging gather/scatter, compaction) run on the TMA engine
+//     (cp.async.bulk through an smem ring, one issuing lane per CTA); HBM<->mapped
+//     pinned host (zero-copy swap) uses 16-byte vector accesses, 8 loads in flight
+//     per thread; both grid-stride over (pair, 32 KB chunk) units.
 // (2) RoPE + paged KV write: the suffix tokens' K/V (miss docs + prompt) are
 //     rotated and scattered straight into their reserved pool blocks, so a
 //     committed node adopts them with no copy (tree.py:252-294 insert_path).
@@ -13,6 +14,7 @@
 #include <cuda_bf16.h>
 
 #include "rcb_internal.h"
+#include "sm100.cuh"
 
 namespace rcb {
 
@@ -80,6 +82,92 @@ __global__ void __launch_bounds__(kCopyThreads)
     copy_unit(src + int64_t(pairs[2 * i]) * block_bytes,
               dst + int64_t(pairs[2 * i + 1]) * block_bytes, block_bytes, c);
   }
+}
+
+// ---------------------------------------------------------------- TMA bulk copy
+// HBM -> HBM block copy on the TMA engine: one elected lane per CTA streams its
+// (pair, 32 KB chunk) units through a kBulkStages-deep smem ring with
+// cp.async.bulk (global -> smem, mbarrier complete_tx) and cp.async.bulk
+// (smem -> global, bulk group).  No data passes through registers; the CTA is one
+// warp.  Device memory on both sides (the zero-copy host path keeps the SIMT kernel).
+constexpr int kBulkChunk = 32768;
+constexpr int kBulkStages = 4;
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src),
+               "r"(bytes)
+               : "memory");
+}
+
+template <bool kByValue>
+__global__ void __launch_bounds__(32)
+    block_copy_bulk_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                           int64_t block_bytes, const __grid_constant__ BlockPairs pairs,
+                           const int32_t* __restrict__ pairs_dev, int n) {
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ __align__(8) uint64_t full[kBulkStages];
+  if (!elect_one()) return;
+  const int64_t cpb = (block_bytes + kBulkChunk - 1) / kBulkChunk;
+  const int64_t units = cpb * n;
+  // this CTA's units: u_k = blockIdx.x + k * gridDim.x
+  const int64_t mine = units > blockIdx.x ? (units - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  for (int s = 0; s < kBulkStages; ++s)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  auto unit = [&](int64_t k, const uint8_t*& s, uint8_t*& d, uint32_t& bytes) {
+    const int64_t u = blockIdx.x + k * gridDim.x;
+    const int i = static_cast<int>(u / cpb);
+    const int64_t c = u - i * cpb;
+    const int32_t ps = kByValue ? pairs.src[i] : pairs_dev[2 * i];
+    const int32_t pd = kByValue ? pairs.dst[i] : pairs_dev[2 * i + 1];
+    const int64_t off = c * kBulkChunk;
+    s = src + int64_t(ps) * block_bytes + off;
+    d = dst + int64_t(pd) * block_bytes + off;
+    const int64_t rem = block_bytes - off;
+    bytes = static_cast<uint32_t>(rem < kBulkChunk ? rem : kBulkChunk);
+  };
+  auto load = [&](int64_t k) {
+    const uint8_t* s;
+    uint8_t* d;
+    uint32_t bytes;
+    unit(k, s, d, bytes);
+    const int st = static_cast<int>(k % kBulkStages);
+    const uint32_t bar = smem_u32(&full[st]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+    bulk_g2s(smem_u32(ring + st * kBulkChunk), s, bytes, bar);
+  };
+  for (int64_t k = 0; k < mine && k < kBulkStages; ++k) load(k);
+  for (int64_t k = 0; k < mine; ++k) {
+    const int st = static_cast<int>(k % kBulkStages);
+    const uint32_t bar = smem_u32(&full[st]);
+    const uint32_t ph = static_cast<uint32_t>((k / kBulkStages) & 1);
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "W_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra W_%=;\n\t}" ::"r"(bar), "r"(ph)
+        : "memory");
+    const uint8_t* s;
+    uint8_t* d;
+    uint32_t bytes;
+    unit(k, s, d, bytes);
+    bulk_s2g(d, smem_u32(ring + st * kBulkChunk), bytes);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    // refill the stage the previous store read from (at most the newest store pending)
+    if (k >= 1 && k - 1 + kBulkStages < mine) {
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      load(k - 1 + kBulkStages);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 int copy_grid(int64_t block_bytes, int n) {
@@ -272,9 +360,59 @@ __global__ void __launch_bounds__(kKvTabThreads)
 
 }  // namespace
 
+#ifndef RCB_BULK_COPY
+#define RCB_BULK_COPY 1
+#endif
+
+namespace {
+// both bases in device memory (not mapped host): the TMA bulk path applies
+bool both_device(const void* a, const void* b) {
+  if (!RCB_BULK_COPY) return false;
+  for (const void* p : {a, b}) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (at.type != cudaMemoryTypeDevice) return false;
+  }
+  return true;
+}
+
+template <bool kByValue>
+cudaError_t launch_bulk(const void* src_base, void* dst_base, int64_t block_bytes,
+                        const BlockPairs* pairs, const int32_t* pairs_dev, int n,
+                        cudaStream_t stream) {
+  static bool attr = false;
+  constexpr int smem = kBulkStages * kBulkChunk;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(block_copy_bulk_kernel<kByValue>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const int64_t units = ((block_bytes + kBulkChunk - 1) / kBulkChunk) * n;
+  const int grid = static_cast<int>(units < sms ? units : sms);  // one CTA per SM (smem)
+  static const BlockPairs kNone{};
+  block_copy_bulk_kernel<kByValue><<<grid, 32, smem, stream>>>(
+      static_cast<const uint8_t*>(src_base), static_cast<uint8_t*>(dst_base), block_bytes,
+      pairs ? *pairs : kNone, pairs_dev, n);
+  return cudaGetLastError();
+}
+}  // namespace
+
 cudaError_t launch_block_copy_params(const void* src_base, void* dst_base, int64_t block_bytes,
                                      const BlockPairs& pairs, int n, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
+  if (both_device(src_base, dst_base))
+    return launch_bulk<true>(src_base, dst_base, block_bytes, &pairs, nullptr, n, stream);
   block_copy_params_kernel<<<copy_grid(block_bytes, n), kCopyThreads, 0, stream>>>(
       static_cast<const uint8_t*>(src_base), static_cast<uint8_t*>(dst_base), block_bytes, pairs,
       n);
@@ -284,6 +422,8 @@ cudaError_t launch_block_copy_params(const void* src_base, void* dst_base, int64
 cudaError_t launch_block_copy_dev(const void* src_base, void* dst_base, int64_t block_bytes,
                                   const int32_t* pairs_dev, int n, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
+  if (both_device(src_base, dst_base))
+    return launch_bulk<false>(src_base, dst_base, block_bytes, nullptr, pairs_dev, n, stream);
   block_copy_dev_kernel<<<copy_grid(block_bytes, n), kCopyThreads, 0, stream>>>(
       static_cast<const uint8_t*>(src_base), static_cast<uint8_t*>(dst_base), block_bytes,
       pairs_dev, n);

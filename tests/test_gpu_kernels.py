@@ -30,7 +30,10 @@ def _pool(nb, L, hkv, bt, hd, seed=0):
 
 
 # ---------------------------------------------------------------- block copy
-@pytest.mark.parametrize("block_bytes,n_pairs", [(32768, 37), (2 * 1024 * 1024, 9), (4096 + 16, 300)])
+# device -> device runs the TMA bulk-copy kernel: a block that is not a whole number of its
+# 32 KB chunks (3 chunks + 48 B), and more units per CTA than ring stages (ring wrap)
+@pytest.mark.parametrize("block_bytes,n_pairs", [(32768, 37), (2 * 1024 * 1024, 9), (4096 + 16, 300),
+                                                 (3 * 32768 + 48, 11), (32768, 2000)])
 def test_block_copy_hbm(block_bytes, n_pairs):
     nb = n_pairs * 2 + 3
     src = torch.randint(0, 256, (nb * block_bytes,), dtype=torch.uint8, device="cuda")

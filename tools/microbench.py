@@ -266,10 +266,11 @@ def bench_attn():
         for mode, qq, qo, tab in (("qkv", x[:, : hq * hd], qr, None),
                                   ("kv_only", None, None, None),
                                   ("kv_only_table", None, None, rope)):
+            mp = int(pos_t.max()) + 1  # outside the timed call (a device sync)
             fn = lambda: kernels.kv_write_rope(qq, k, v, qo, pos_t, slots, pool.data_ptr(),
                                                block_tokens=bt, n_layers=L, n_kv_heads=hkv,
                                                head_dim=hd, layer=1, rope_theta=1e6, n_q_heads=hq,
-                                               rope=tab, max_pos=int(pos_t.max()) + 1)
+                                               rope=tab, max_pos=mp)
             med, best = timed(fn)
             nbytes = T * hd * 2 * (2 * hkv * 2 + (2 * hq if qq is not None else 0))
             emit(kind="kv_write_rope", mode=mode, case=name, ms=med, gbs=nbytes / med / 1e6)

@@ -120,7 +120,7 @@ struct Smem {
 // O of a full query tile leaves through a TMA store staged in the finished item's Q
 // buffer (its last QK retired before the last PV, i.e. before O_w was complete); the
 // epilogue's arrival on Q_empty then releases the buffer for Q(ii + 2).  Ragged tiles and
-// split-KV parts keep the per-lane stores.
+// split-KV parts keep the per-lane stores, and so do G <= 2 launches (kStageO below).
 constexpr bool kOTma = RCB_OTMA != 0;
 constexpr int kItemInts = 8;
 struct Item {
@@ -176,6 +176,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                           float* __restrict__ part_o, float2* __restrict__ part_ml) {
   using S = Smem<HD, BT, SPLIT>;
   constexpr int TQ = kRows / G;  // tokens per query tile
+  // O through the Q buffer + TMA store for G > 2 only.  Q(ii + 2) then lands only after item
+  // ii's O left the buffer, and with fused RoPE it must still be rotated before item ii + 2
+  // starts: MHA items are short (2-5 KV steps at 128 tokens per tile), so that chain stalls
+  // the MMA warp (LLaMA2 miss batch with fused RoPE 117.8 -> 107.5 and 121.9 -> 109.6 us with
+  // direct stores, two A/B runs), while GQA-4 gains from the staging (Mistral mixed step
+  // 480.8 -> 501.7 us without it)
+  constexpr bool kStageO = kOTma && G > 2;
   constexpr int BPT = S::kBPT;
   constexpr int NS = S::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -195,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bar[kQFull0 + b], 1);
-      mbar_init(&bar[kQEmpty0 + b], kOTma ? 2 : 1);  // MMA (last QK) + epilogue (O store)
+      mbar_init(&bar[kQEmpty0 + b], kStageO ? 2 : 1);  // MMA (last QK) + epilogue (O store)
       mbar_init(&bar[kQReady0 + b], kRows);
       mbar_init(&bar[kSFull0 + b], 1);
       mbar_init(&bar[kPFull0 + b], kRows);
@@ -744,7 +751,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int tok = (2 * it.qp + qt) * TQ + t_local;
       const bool row_valid = tok < it.q_len;
       // a full tile (every token valid) is staged in its Q buffer and TMA-stored
-      const bool stage = kOTma && !SPLIT && (2 * it.qp + qt + 1) * TQ <= it.q_len;
+      const bool stage = kStageO && !SPLIT && (2 * it.qp + qt + 1) * TQ <= it.q_len;
       const uint32_t stg = smem_u32(sQ) + (qb * S::kQT + (SPLIT ? 0 : qt)) * S::kQ;
       float2 ml0 = make_float2(-INFINITY, 0.f), ml1 = ml0;
       if (use0) {
@@ -864,13 +871,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         epilogue(it, 0, true, false, ii & 1, ii);
         if (it.has(1)) epilogue(it, 1, false, true, ii & 1, ii);
       }
-      if (kOTma && row == 0) {  // the staged O left smem: Q(ii + 2) may land in the buffer
+      if (kStageO && row == 0) {  // the staged O left smem: Q(ii + 2) may land in the buffer
         tma_store_wait_read();
         mbar_arrive(&bar[kQEmpty0 + (ii & 1)]);
       }
       if (rope != nullptr && ii + kAhead < n_mine) rotate_q(item_of(ii + kAhead), ii + kAhead);
     }
-    if (kOTma && row == 0) tma_store_wait_all();
+    if (kStageO && row == 0) tma_store_wait_all();
     tc_fence_before();
   }
   __syncthreads();

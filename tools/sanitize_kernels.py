@@ -62,6 +62,9 @@ def main():
     # split-KV parts + combine
     errs["gqa_rope"] = attention(32, 8, 128, 64, [([200], [300, 32]), ([], [160])], rope=True)
     errs["mha"] = attention(8, 8, 128, 32, [([64], [130])], rope=False)
+    # MHA with fused RoPE: direct O stores, Q(ii+2) landing right after item ii's last QK
+    errs["mha_rope"] = attention(4, 4, 128, 64, [([], [544]), ([128], [300]), ([], [130])],
+                                 rope=True)
     errs["decode"] = attention(32, 8, 128, 64, [([500], [1]), ([300], [1])], rope=True)
     errs["split_kv"] = attention(8, 1, 128, 64, [([1500], [1])], rope=False, split_kv=True)
     # retrieval scan + merge, shard merge
@@ -74,6 +77,15 @@ def main():
     assert [tuple(r) for r in ids[:, -1].cpu().tolist()] == docs
     m_ids, _ = kernels.topk_merge_shards(torch.stack([ids, ids]), torch.stack([sc, sc]))
     assert torch.equal(m_ids[:, -1], ids[:, -1])
+    # HBM -> HBM block copy (TMA bulk kernel), ragged last chunk, ring wrap
+    bb, npairs = 3 * 32768 + 48, 40
+    src = torch.randint(0, 256, (2 * npairs * bb,), dtype=torch.uint8, device="cuda")
+    dst = torch.zeros_like(src)
+    pr = torch.stack([torch.arange(npairs), torch.arange(2 * npairs - 1, npairs - 1, -1)], 1)
+    kernels.block_copy(src.data_ptr(), dst.data_ptr(), bb, pr.to(torch.int32).cuda())
+    torch.cuda.synchronize()
+    sv, dv = src.view(2 * npairs, bb), dst.view(2 * npairs, bb)
+    assert torch.equal(sv[pr[:, 0].cuda()], dv[pr[:, 1].cuda()])
     # K/V write (table-driven) + pool swaps (staged gather/scatter kernels + DMA)
     bt, L, hkv, hd = 16, 2, 4, 64
     pool_t = torch.zeros((32, L, 2, hkv, bt, hd), dtype=torch.bfloat16, device="cuda")

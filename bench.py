@@ -435,7 +435,7 @@ def run_ours(args, dist: Dist):
     return result
 
 
-def measure_timed(w, qw, prof, decode_ms, stage_ms, pcie) -> dict:
+def measure_timed(w, qw, prof, decode_ms, stage_ms, pcie, max_rate: float = 400.0) -> dict:
     """Hardware-in-the-loop curves (every admitted prefill executed on the GPU, TimedEngine):
     TTFT vs hit rate over 4 GPU tiers and req/s at the 5x TTFT SLO on the repeated-question
     variant of this workload, plus configs[2] (LLaMA2-7B top-5, two tiers) with real
@@ -465,7 +465,7 @@ def measure_timed(w, qw, prof, decode_ms, stage_ms, pcie) -> dict:
             out["req_per_s_at_5x_slo"] = {
                 "workload": qw.name, "how": "ragsim's measure_throughput bisection "
                 "(simulator.py:648-681), every probe a timed run",
-                "points": [timed_slo_throughput(runner, cap, n_requests=300, **kw)
+                "points": [timed_slo_throughput(runner, cap, n_requests=300, max_rate=max_rate, **kw)
                            for cap in (tiers[0], tiers[-1])]}
             runner.close()
     c2 = WORKLOADS["llama2-7b-top5-qpool"]
@@ -516,7 +516,10 @@ def measure_ttft(w, swap, stage_ms: float, timed_on: bool = True) -> dict:
                              host_tier=qw.host_capacity_tokens, pcie_gbs=pcie,
                              decode_ms_per_token=decode_ms)
         slo_s = time.perf_counter() - t1
-    timed = measure_timed(w, qw, prof, decode_ms, stage_ms, pcie) if timed_on else None
+    # the timed bisection's upper bracket: twice the profile-driven rate (its 7 halvings then
+    # resolve ~0.5 req/s instead of ~3 from ragsim's default 400 req/s bracket)
+    hi = 2.0 * max((p["req_per_s_at_slo"] for p in slo), default=200.0)
+    timed = measure_timed(w, qw, prof, decode_ms, stage_ms, pcie, max_rate=hi) if timed_on else None
     idx = {(a, b): prof.times[i][j] for i, a in enumerate(prof.alpha_grid)
            for j, b in enumerate(prof.beta_grid)}
     return {"timed": timed, "p50_ttft_ms": own["p50_ttft_ms"], "mean_ttft_ms": own["mean_ttft_ms"],

@@ -29,13 +29,51 @@ def _stream(stream) -> int:
     return _lib.stream_handle(stream)
 
 
+class _PinnedRing:
+    """Reusable pinned staging buffers for the per-step host -> device uploads (block
+    tables, work lists, slot maps).  ``Tensor.pin_memory()`` per upload goes through the
+    caching host allocator, which cannot reuse a block while its copy is in flight and
+    falls back to cudaHostAlloc (milliseconds, and it can serialise with the device);
+    here a buffer is reused once the event recorded after its last copy has completed,
+    and grows (power of two) only when an upload outgrows it."""
+
+    def __init__(self, depth: int = 8) -> None:
+        self.bufs: list[torch.Tensor | None] = [None] * depth
+        self.events: list[torch.cuda.Event | None] = [None] * depth
+        self.i = 0
+
+    def upload(self, t: torch.Tensor, device) -> torch.Tensor:
+        i = self.i
+        self.i = (i + 1) % len(self.bufs)
+        if self.events[i] is not None:
+            self.events[i].synchronize()  # its previous copy has left the buffer
+        n = t.numel() * t.element_size()
+        buf = self.bufs[i]
+        if buf is None or buf.numel() < n:
+            buf = torch.empty(max(1 << 16, 1 << (n - 1).bit_length()), dtype=torch.uint8).pin_memory()
+            self.bufs[i] = buf
+        host = buf[:n].view(t.dtype).view(t.shape)
+        host.copy_(t)
+        out = host.to(device, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self.events[i] = ev
+        return out
+
+
+_ring: _PinnedRing | None = None
+
+
 def _upload(arr: np.ndarray, device) -> torch.Tensor:
     """Host array -> device without a stream sync: a pageable copy would wait for the
     work already queued (e.g. the previous step's prefill) before returning."""
-    t = torch.from_numpy(arr)
+    global _ring
+    t = torch.from_numpy(np.ascontiguousarray(arr))
     if torch.device(device).type != "cuda":
         return t.to(device)
-    return t.pin_memory().to(device, non_blocking=True)
+    if _ring is None:
+        _ring = _PinnedRing()
+    return _ring.upload(t, device)
 
 
 def block_copy(src_base: int, dst_base: int, block_bytes: int, pairs: torch.Tensor,

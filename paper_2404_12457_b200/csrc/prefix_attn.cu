@@ -56,9 +56,11 @@ constexpr int kPoly16 = RCB_POLY16;  // of every 16 columns (even)
 //   producer, step s: [s][16] block ids loaded, [17] K(s) issued, [18] V(s) issued
 //   epilogue, item ii: [ii][19] O0 full seen, [20] O0 freed, [21] O1 full seen, [22] O1 freed,
 //   [23] item's O written (stores issued)
+//   softmax WG w, its tile c, chunk ch: [c][24 + 4w + 2ch] S chunk in registers,
+//   [25 + 4w + 2ch] exp loop done (before the bf16 pack + TMEM store)
 #ifdef RCB_TRACE
 constexpr int kTraceTiles = 1024;
-constexpr int kTraceEv = 24;
+constexpr int kTraceEv = 32;
 __device__ long long g_trace[kTraceTiles * kTraceEv];
 #define TRACE(g, ev)                                                                      \
   do {                                                                                    \
@@ -534,6 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = 0; i < kKeys / 2; ++i) s[i] = __uint_as_float(r[i]);
           }
+          if (tr) TRACE(c, 24 + 4 * wg + 2 * ch);
           if (masked) {
             // keys valid in block b for this row: off < min(valid_b, qp - pos_b + 1)
 #pragma unroll
@@ -605,6 +608,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               acc1 = fadd2(acc1, f2_pack(s[i + e + 2], s[i + e + 3]));
             }
           }
+          if (tr) TRACE(c, 25 + 4 * wg + 2 * ch);
           float a0, a1, b0, b1;
           f2_unpack(acc0, a0, a1);
           f2_unpack(acc1, b0, b1);

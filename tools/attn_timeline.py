@@ -20,7 +20,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2404_12457_b200 import _lib, kernels  # noqa: E402
 
-EV = 24
+EV = 32
 TILES = 1024
 CASES = {
     "mistral_miss": (32, 8, [(0, 1056)] * 16),
@@ -98,6 +98,22 @@ def main():
         print(f"QK0 issued -> S0 seen median {np.median(tr[1:k, 1] - tr[1:k, 9]):.0f}, "
               f"S0 seen -> P0 arrive (softmax, both chunks) {np.median(tr[1:k, 2] - tr[1:k, 1]):.0f}, "
               f"S1 seen -> P1 arrive {np.median(tr[1:k, 6] - tr[1:k, 5]):.0f}")
+    # softmax breakdown (WG 0 and 1): S seen -> chunk 0 in registers -> exp done -> P0 arrive
+    # -> chunk 1 in registers -> exp done -> P arrive (tile done)
+    k = min(len(qk0), TILES) - 2
+    for w in (0, 1):
+        t = tr[1:k]
+        ok = (t[:, 4 * w + 1] > 0) & (t[:, 24 + 4 * w] > 0) & (t[:, 4 * w + 2] > 0)
+        t = t[ok]
+        if len(t):
+            d = lambda a, b: np.median(t[:, b] - t[:, a])  # noqa: E731
+            c1 = t[:, 26 + 4 * w] > 0
+            print(f"WG{w} softmax (median cycles, n={len(t)}): S seen -> chunk0 in regs "
+                  f"{d(4 * w + 1, 24 + 4 * w):.0f}, -> exp0 done {d(24 + 4 * w, 25 + 4 * w):.0f}, "
+                  f"chunk1 ld {np.median(t[c1, 26 + 4 * w] - t[c1, 25 + 4 * w]):.0f} "
+                  f"(incl. pack/st/arrive of chunk 0), -> exp1 done "
+                  f"{np.median(t[c1, 27 + 4 * w] - t[c1, 26 + 4 * w]):.0f}, -> P arrive "
+                  f"{np.median(t[c1, 4 * w + 2] - t[c1, 27 + 4 * w]):.0f}; total {d(4 * w + 1, 4 * w + 2):.0f}")
     print(f"QK-to-QK cycles: inside items median {np.median(inside):.0f} (n={len(inside)}), "
           f"into an item's first step median {np.median(boundary):.0f} (n={len(boundary)})")
 

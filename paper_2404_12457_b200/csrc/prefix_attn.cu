@@ -49,6 +49,10 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #endif
 constexpr int kPoly16 = RCB_POLY16;  // of every 16 columns (even)
 
+// TMEM load of one O chunk, 32 or 16 columns (the epilogue's chunk width depends on G)
+__device__ __forceinline__ void tmem_ldn(uint32_t taddr, uint32_t (&r)[32]) { tmem_ld32(taddr, r); }
+__device__ __forceinline__ void tmem_ldn(uint32_t taddr, uint32_t (&r)[16]) { tmem_ld16(taddr, r); }
+
 // Per-step handoff timestamps of CTA 0 (debug builds with -DRCB_TRACE only; tools/attn_trace.py)
 //   softmax WG w, its tile c: [c][4w + 0] S wait start, [4w + 1] S seen, [4w + 2] P arrive
 //   MMA, step s: [s][8] P0 seen, [9] QK0 issued, [10] P1 seen, [11] QK1 issued,
@@ -185,6 +189,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   // direct stores, two A/B runs), while GQA-4 gains from the staging (Mistral mixed step
   // 480.8 -> 501.7 us without it)
   constexpr bool kStageO = kOTma && G > 2;
+  // O columns the epilogue drains per TMEM load.  16 for G <= 2: the smaller register
+  // footprint of the drain (MHA: no staging, rotation every item) measured LLaMA2 miss
+  // batch with RoPE 103.5 -> 99.3 us; GQA-4 keeps 32 (hit batch 72.7 vs 74.7 us with 16)
+  constexpr int kOCols = G <= 2 ? 16 : 32;
   constexpr int BPT = S::kBPT;
   constexpr int NS = S::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -786,20 +794,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       __nv_bfloat16* orow =
           out + (static_cast<int64_t>(it.q_start + tok) * n_q_heads + it.kvh * G + h_local) * HD;
 #pragma unroll 1
-      for (int ch = 0; ch < HD / 32; ++ch) {
-        uint32_t r0[32], r1[32];
-        if (use0) tmem_ld32(t_row + 256 + ch * 32, r0);
-        if (use1) tmem_ld32(t_row + 384 + ch * 32, r1);
+      for (int ch = 0; ch < HD / kOCols; ++ch) {
+        uint32_t r0[kOCols], r1[kOCols];
+        if (use0) tmem_ldn(t_row + 256 + ch * kOCols, r0);
+        if (use1) tmem_ldn(t_row + 384 + ch * kOCols, r1);
         tmem_wait_ld();
-        if (ch == HD / 32 - 1) {  // O is in registers: release it to the next item
+        if (ch == HD / kOCols - 1) {  // O is in registers: release it to the next item
           tc_fence_before();
           if (use0) mbar_arrive(&bar[kOFree0 + 0]);
           if (use1) mbar_arrive(&bar[kOFree0 + 1]);
           if (row == 0) TRACE(ii, use0 ? 20 : 22);
         }
-        float o[32];
+        float o[kOCols];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
+        for (int i = 0; i < kOCols; ++i) {
           const float a = use0 ? __uint_as_float(r0[i]) * c0 : 0.f;
           o[i] = use1 ? fmaf(__uint_as_float(r1[i]), c1, a) : a;
         }
@@ -809,19 +817,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         // sharing the SM sub-partitions (trace: -18% cycles per KV step without it)
         if (part) {
           if (!row_valid) continue;  // rows past q_len: nothing to combine
-          float* prow = part_o + (static_cast<int64_t>(it.ps) * kRows + row) * HD + ch * 32;
+          float* prow = part_o + (static_cast<int64_t>(it.ps) * kRows + row) * HD + ch * kOCols;
 #pragma unroll
-          for (int i = 0; i < 32; i += 8)
+          for (int i = 0; i < kOCols; i += 8)
             asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
                          :: "l"(prow + i), "f"(o[i]), "f"(o[i + 1]), "f"(o[i + 2]), "f"(o[i + 3]),
                             "f"(o[i + 4]), "f"(o[i + 5]), "f"(o[i + 6]), "f"(o[i + 7])
                          : "memory");
         } else if (stage) {
           // SW128 Q-tile layout: [half][row][128 B], 16-byte chunk c of row r at (c ^ (r & 7))
-          const uint32_t rb = stg + (ch >> 1) * 16384 + (row >> 3) * 1024 + (row & 7) * 128;
+          const int col0 = ch * kOCols;
+          const uint32_t rb = stg + (col0 >> 6) * 16384 + (row >> 3) * 1024 + (row & 7) * 128;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int c16 = (ch & 1) * 4 + k;
+          for (int k = 0; k < kOCols / 8; ++k) {
+            const int c16 = ((col0 & 63) >> 3) + k;
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};"
                          :: "r"(rb + ((c16 ^ (row & 7)) << 4)),
                             "r"(pack_bf16(o[8 * k + 0], o[8 * k + 1])),
@@ -832,12 +841,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else if (row_valid) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 16) {
+          for (int i = 0; i < kOCols; i += 16) {
             uint32_t v[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) v[e] = pack_bf16(o[i + 2 * e], o[i + 2 * e + 1]);
             asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
-                         :: "l"(orow + ch * 32 + i), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]),
+                         :: "l"(orow + ch * kOCols + i), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]),
                             "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
                          : "memory");
           }

@@ -424,6 +424,7 @@ def run_ours(args, dist: Dist):
                           "frac": round(scan_gbs / hbm_peak, 4),
                           "call_ms_mean": round(sum(scan_ms) / max(1, len(scan_ms)), 4),
                           "passes_per_step": n_passes,
+                          "shard_exchange": retr.exchange,
                           "how": "device_ms: the first timed step's queries, 20 local scans "
                                  "(scan + merge kernels per pass) replayed from a CUDA graph, "
                                  "CUDA events; call_ms_mean: in-step event pair around the "

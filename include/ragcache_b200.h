@@ -234,6 +234,29 @@ int rcb_topk_merge_shards(const int64_t* ids_in_dev, const float* scores_in_dev,
                           int32_t n_shards, int32_t n_queries, int32_t n_stages, int32_t k,
                           int64_t* ids_out_dev, float* scores_out_dev, void* stream);
 
+/* ---- peer-memory list exchange (replaces the two list allGathers above).
+ * Each rank allocates an exchange window, exports it with a CUDA IPC handle and opens
+ * every peer's (NVLink P2P on one box).  Per retrieval call with epoch e = 1, 2, ...:
+ * rcb_peer_push writes this rank's [n_queries][n_stages][k] lists into slot (e&1, rank)
+ * of every window and publishes e in each window's flags[rank] (system-scope release);
+ * rcb_peer_merge waits (acquire, bounded by timeout_ns: *timed_out_dev = 1 instead of a
+ * hang) for every rank's flag and merges its own window's slot (e&1).  A rank may push
+ * e+1 only after every rank issued its epoch-e merge (the step's query allGather orders
+ * it).  Replaces: the NCCL merge of retrieval_topk(..., ncclComm_t) in SURVEY §8b. */
+#define RCB_PEER_HANDLE_BYTES 64
+int64_t rcb_peer_window_bytes(int32_t n_ranks, int64_t n_entries);
+int rcb_peer_window_alloc(int32_t n_ranks, int64_t n_entries, void** window_out);
+int rcb_peer_window_free(void* window);
+int rcb_peer_ipc_handle(void* window, void* handle_out);
+int rcb_peer_open(const void* handle, void** window_out);
+int rcb_peer_close(void* window);
+int rcb_peer_push(void* const* windows, int32_t n_ranks, int32_t rank, int64_t n_entries,
+                  const int64_t* ids_dev, const float* scores_dev, uint32_t epoch,
+                  void* stream);
+int rcb_peer_merge(const void* window, int32_t n_ranks, int32_t n_queries, int32_t n_stages,
+                   int32_t k, uint32_t epoch, uint64_t timeout_ns, int32_t* timed_out_dev,
+                   int64_t* ids_out_dev, float* scores_out_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

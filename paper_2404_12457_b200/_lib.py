@@ -11,7 +11,7 @@ from __future__ import annotations
 
 import ctypes
 import os
-from ctypes import POINTER, c_char_p, c_float, c_int, c_int32, c_int64, c_void_p
+from ctypes import POINTER, c_char_p, c_float, c_int, c_int32, c_int64, c_uint32, c_uint64, c_void_p
 
 LIB_NAME = "libragcache_b200.so"
 # RCB_LIB_PATH selects an alternate in-tree build (A/B kernel experiments only)
@@ -23,6 +23,7 @@ RCB_ERR_NO_BLOCKS = 1
 RCB_ERR_BAD_HANDLE = 2
 RCB_ERR_CUDA = 3
 RCB_ERR_ARG = 4
+RCB_PEER_HANDLE_BYTES = 64
 
 RCB_TIER_GPU = 0
 RCB_TIER_HOST = 1
@@ -104,6 +105,16 @@ SIGNATURES = [
                                      c_void_p]),
     ("rcb_topk_merge_shards", c_int, [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int32,
                                       c_void_p, c_void_p, c_void_p]),
+    ("rcb_peer_window_bytes", c_int64, [c_int32, c_int64]),
+    ("rcb_peer_window_alloc", c_int, [c_int32, c_int64, POINTER(c_void_p)]),
+    ("rcb_peer_window_free", c_int, [c_void_p]),
+    ("rcb_peer_ipc_handle", c_int, [c_void_p, c_void_p]),
+    ("rcb_peer_open", c_int, [c_void_p, POINTER(c_void_p)]),
+    ("rcb_peer_close", c_int, [c_void_p]),
+    ("rcb_peer_push", c_int, [POINTER(c_void_p), c_int32, c_int32, c_int64, c_void_p, c_void_p,
+                              c_uint32, c_void_p]),
+    ("rcb_peer_merge", c_int, [c_void_p, c_int32, c_int32, c_int32, c_int32, c_uint32, c_uint64,
+                               c_void_p, c_void_p, c_void_p, c_void_p]),
 ]
 
 _lib: ctypes.CDLL | None = None

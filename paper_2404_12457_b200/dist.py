@@ -77,6 +77,14 @@ class Dist:
         self.pg.all_gather_into_tensor(out, t.contiguous().reshape(-1))  # one buffer, no stack
         return out.view((self.world,) + tuple(t.shape))
 
+    def all_gather_object(self, obj) -> list:
+        """Picklable object of every rank, rank order (setup-time exchanges)."""
+        if self.pg is None:
+            return [obj]
+        out = [None] * self.world
+        self.pg.all_gather_object(out, obj)
+        return out
+
     def close(self) -> None:
         if self.pg is not None:
             self.pg.destroy_process_group()

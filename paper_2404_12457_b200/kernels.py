@@ -7,6 +7,7 @@ missing library raises RcbUnavailable, a non-CUDA tensor raises ValueError.
 
 from __future__ import annotations
 
+import ctypes
 import math
 import os
 
@@ -370,3 +371,76 @@ def topk_merge_shards(ids: torch.Tensor, scores: torch.Tensor, stream=None):
                                        _dev_ptr(ids_out), _dev_ptr(sc_out), _stream(stream)),
           "rcb_topk_merge_shards")
     return ids_out, sc_out
+
+
+class PeerExchange:
+    """Peer-memory exchange of the per-shard staged lists (rcb_peer_*, csrc/peer.cu).
+
+    Each rank allocates an exchange window, exports it as a CUDA IPC handle, all-gathers
+    the handles once (``comm.all_gather_object``) and maps every peer's window (NVLink P2P
+    on one box; the same memory when ranks share a GPU).  ``merge(ids, scores)`` pushes this
+    rank's [n_queries, S, k] lists into slot (epoch & 1, rank) of every window, publishes the
+    epoch, waits for all ranks' epochs and merges its own window: one push + one merge kernel
+    instead of two all-gathers + the merge.  The caller orders successive calls with a
+    collective between them (ShardedRetriever's query all-gather).
+    """
+
+    def __init__(self, comm, n_queries: int, n_stages: int, k: int, timeout_s: float = 10.0,
+                 device="cuda") -> None:
+        lib = load()
+        self.lib = lib
+        self.R, self.rank = comm.world, comm.rank
+        self.nq, self.S, self.k = n_queries, n_stages, k
+        self.E = n_queries * n_stages * k
+        self.timeout_ns = int(timeout_s * 1e9)
+        win = ctypes.c_void_p()
+        check(lib.rcb_peer_window_alloc(self.R, self.E, ctypes.byref(win)), "rcb_peer_window_alloc")
+        self.own = win.value
+        self.opened = []
+        try:
+            h = (ctypes.c_uint8 * _lib.RCB_PEER_HANDLE_BYTES)()
+            check(lib.rcb_peer_ipc_handle(self.own, h), "rcb_peer_ipc_handle")
+            handles = comm.all_gather_object(bytes(h))
+            wins = []
+            for r, hb in enumerate(handles):
+                if r == self.rank:
+                    wins.append(self.own)
+                    continue
+                p = ctypes.c_void_p()
+                buf = (ctypes.c_uint8 * len(hb)).from_buffer_copy(hb)
+                check(lib.rcb_peer_open(buf, ctypes.byref(p)), "rcb_peer_open")
+                self.opened.append(p.value)
+                wins.append(p.value)
+        except Exception:
+            self.close()
+            raise
+        self.windows = (ctypes.c_void_p * self.R)(*wins)
+        self.epoch = 0
+        self.timed_out = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def merge(self, ids: torch.Tensor, scores: torch.Tensor, stream=None):
+        """ids int64 / scores f32 [n_queries, S, k] of this rank's shard -> merged lists."""
+        assert ids.shape == (self.nq, self.S, self.k) and ids.is_contiguous() and scores.is_contiguous()
+        self.epoch += 1
+        st = _stream(stream)
+        check(self.lib.rcb_peer_push(self.windows, self.R, self.rank, self.E, _dev_ptr(ids),
+                                     _dev_ptr(scores), self.epoch, st), "rcb_peer_push")
+        ids_out = torch.empty_like(ids)
+        sc_out = torch.empty_like(scores)
+        check(self.lib.rcb_peer_merge(self.own, self.R, self.nq, self.S, self.k, self.epoch,
+                                      self.timeout_ns, _dev_ptr(self.timed_out),
+                                      _dev_ptr(ids_out), _dev_ptr(sc_out), st), "rcb_peer_merge")
+        return ids_out, sc_out
+
+    def check_timeout(self) -> None:
+        """Raise if any merge gave up waiting for a peer (reads a device flag: syncs)."""
+        if int(self.timed_out.item()):
+            raise RuntimeError("peer exchange: a rank's lists did not arrive within the timeout")
+
+    def close(self) -> None:
+        for p in self.opened:
+            self.lib.rcb_peer_close(ctypes.c_void_p(p))
+        self.opened = []
+        if self.own:
+            self.lib.rcb_peer_window_free(ctypes.c_void_p(self.own))
+            self.own = None

@@ -46,11 +46,16 @@ class ShardedRetriever:
                   equal-sized blocks)
     scan / merge  the kernels by default; tests on CPU inject the oracle to
                   exercise the collective logic without a GPU
+    exchange      how the per-shard lists meet (world > 1): "p2p" = kernels.PeerExchange
+                  (each rank pushes its lists into every peer's window over peer memory,
+                  one merge kernel waits for all of them), "allgather" = two collective
+                  all-gathers + the merge kernel; "auto" = p2p for device tensors with the
+                  kernel merge, falling back to allgather if the IPC setup fails
     """
 
     def __init__(self, corpus_shard, id_offset: int, k: int, n_stages: int, comm=None, *,
                  batch: int = MAX_BATCH, pass_queries: int | None = None, scan=None,
-                 merge=None) -> None:
+                 merge=None, exchange: str = "auto") -> None:
         self.corpus = corpus_shard
         self.off = int(id_offset)
         self.k = k
@@ -76,6 +81,21 @@ class ShardedRetriever:
         self._qpad = torch.zeros((batch, corpus_shard.shape[1]), dtype=torch.bfloat16, device=dev)
         self.launches = 0
         self.bytes_per_scan = corpus_shard.shape[0] * corpus_shard.shape[1] * 2
+        self.px = None
+        self.exchange = "allgather" if self.world == 1 else exchange
+        if self.world > 1 and exchange in ("auto", "p2p"):
+            if merge is None and dev.type == "cuda":
+                try:
+                    self.px = kernels.PeerExchange(comm, nq, n_stages, k, device=dev)
+                    self.exchange = "p2p"
+                except RuntimeError as exc:  # CUDA IPC / peer mapping unavailable on this box
+                    if exchange == "p2p":
+                        raise
+                    self.exchange = f"allgather (peer exchange unavailable: {exc})"
+            elif exchange == "p2p":
+                raise ValueError("p2p exchange needs device tensors and the kernel merge")
+            else:
+                self.exchange = "allgather"
 
     def _scan_pass(self, q, a, b):
         if self._scan is not None:
@@ -104,12 +124,18 @@ class ShardedRetriever:
         if self.world == 1:
             self.scan_all(q_local)
             return (self.ids[:b], self.sc[:b]) if with_scores else self.ids[:b]
+        # the query all-gather also orders successive peer exchanges (every rank has issued
+        # the previous merge before any rank pushes the next lists)
         allq = self.comm.all_gather(q_local).reshape(-1, q_local.shape[1])
         self.scan_all(allq)
-        gi = self.comm.all_gather(self.ids)  # [world, world*batch, S, k]
-        gs = self.comm.all_gather(self.sc)
-        ids, sc = self._merge(gi, gs)
-        self.launches += 1
+        if self.px is not None:
+            ids, sc = self.px.merge(self.ids, self.sc)
+            self.launches += 3  # push, wait, merge
+        else:
+            gi = self.comm.all_gather(self.ids)  # [world, world*batch, S, k]
+            gs = self.comm.all_gather(self.sc)
+            ids, sc = self._merge(gi, gs)
+            self.launches += 1
         r0 = self.rank * self.batch
         return (ids[r0:r0 + b], sc[r0:r0 + b]) if with_scores else ids[r0:r0 + b]
 

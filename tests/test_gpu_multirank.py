@@ -47,3 +47,17 @@ def test_two_rank_sharded_stage_provider_on_one_gpu():
     for r in rows:
         assert r["identical"] and r["finals_equal_unsharded"], r
         assert r["speculations"] > 0 and r["requests"] > 0
+
+
+def test_two_rank_peer_exchange_matches_allgather():
+    """The per-shard lists meet over peer memory (CUDA IPC windows, push + epoch flags +
+    device merge): bit-identical to the all-gather exchange over several calls."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29545",
+           os.path.join("tests", "peer_exchange_run.py")]
+    res = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-3000:]
+    rows = [json.loads(l) for l in res.stdout.splitlines() if l.startswith("{")]
+    assert sorted(r["rank"] for r in rows) == [0, 1]
+    for r in rows:
+        assert r["exchange"] == "p2p" and r["identical"] and r["epoch"] == r["calls"], r

@@ -353,6 +353,7 @@ def run_ours(args, dist: Dist):
     dev_scan_ms = retr.device_ms(q_block)
     scan_bytes = retr.bytes_per_scan
     n_passes = len(retr.passes)
+    shard_exchange = retr.exchange
     scan_gbs = scan_bytes / (dev_scan_ms / 1e3) / 1e9
     d2h = st1["d2h_bytes"] - st0["d2h_bytes"]
     h2d = st1["h2d_bytes"] - st0["h2d_bytes"]
@@ -424,7 +425,7 @@ def run_ours(args, dist: Dist):
                           "frac": round(scan_gbs / hbm_peak, 4),
                           "call_ms_mean": round(sum(scan_ms) / max(1, len(scan_ms)), 4),
                           "passes_per_step": n_passes,
-                          "shard_exchange": retr.exchange,
+                          "shard_exchange": shard_exchange,
                           "how": "device_ms: the first timed step's queries, 20 local scans "
                                  "(scan + merge kernels per pass) replayed from a CUDA graph, "
                                  "CUDA events; call_ms_mean: in-step event pair around the "

@@ -256,6 +256,15 @@ int rcb_peer_push(void* const* windows, int32_t n_ranks, int32_t rank, int64_t n
 int rcb_peer_merge(const void* window, int32_t n_ranks, int32_t n_queries, int32_t n_stages,
                    int32_t k, uint32_t epoch, uint64_t timeout_ns, int32_t* timed_out_dev,
                    int64_t* ids_out_dev, float* scores_out_dev, void* stream);
+/* the same window as a raw all-gather (the step's queries): rcb_peer_push_bytes copies
+ * `bytes` (multiple of 8, <= 8 * n_entries) into the ids-region slot (e&1, rank) of every
+ * window and publishes e; after rcb_peer_wait the gathered rows of all ranks are contiguous
+ * at window + rcb_peer_slot_offset(n_ranks, n_entries, e), rank r at r * 8 * n_entries */
+int rcb_peer_push_bytes(void* const* windows, int32_t n_ranks, int32_t rank, int64_t n_entries,
+                        const void* src_dev, int64_t bytes, uint32_t epoch, void* stream);
+int rcb_peer_wait(const void* window, int32_t n_ranks, int64_t n_entries, uint32_t epoch,
+                  uint64_t timeout_ns, int32_t* timed_out_dev, void* stream);
+int64_t rcb_peer_slot_offset(int32_t n_ranks, int64_t n_entries, uint32_t epoch);
 
 #ifdef __cplusplus
 }

@@ -115,6 +115,10 @@ SIGNATURES = [
                               c_uint32, c_void_p]),
     ("rcb_peer_merge", c_int, [c_void_p, c_int32, c_int32, c_int32, c_int32, c_uint32, c_uint64,
                                c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("rcb_peer_push_bytes", c_int, [POINTER(c_void_p), c_int32, c_int32, c_int64, c_void_p,
+                                    c_int64, c_uint32, c_void_p]),
+    ("rcb_peer_wait", c_int, [c_void_p, c_int32, c_int64, c_uint32, c_uint64, c_void_p, c_void_p]),
+    ("rcb_peer_slot_offset", c_int64, [c_int32, c_int64, c_uint32]),
 ]
 
 _lib: ctypes.CDLL | None = None

@@ -65,6 +65,24 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// generic form: copy `bytes` (a multiple of 8) into the ids region slot [parity][rank] of
+// destination p, then publish the epoch (the query exchange uses it for bf16 rows)
+__global__ void __launch_bounds__(256)
+    push_bytes_kernel(Windows win, int n_ranks, int rank, int64_t n_entries,
+                      const long long* __restrict__ src, int64_t words, unsigned epoch) {
+  const int p = blockIdx.x;
+  const Layout l = layout(n_ranks, n_entries);
+  uint8_t* w = win.w[p];
+  long long* d = reinterpret_cast<long long*>(w + l.ids) + (int64_t(epoch & 1) * n_ranks + rank) * n_entries;
+  for (int64_t i = threadIdx.x; i < words; i += blockDim.x) d[i] = src[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    unsigned* f = reinterpret_cast<unsigned*>(w + l.flags) + rank;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+  }
+}
+
 // one thread: wait (acquire) until every sender published `epoch`; bounded, so a missing
 // peer sets *timed_out instead of hanging the device
 __global__ void wait_kernel(const uint8_t* __restrict__ window, int n_ranks, int64_t n_entries,
@@ -179,6 +197,38 @@ int rcb_peer_merge(const void* window, int32_t n_ranks, int32_t n_queries, int32
   return rcb_topk_merge_shards(reinterpret_cast<const int64_t*>(w + l.ids) + slot,
                                reinterpret_cast<const float*>(w + l.scores) + slot, n_ranks,
                                n_queries, n_stages, k, ids_out_dev, scores_out_dev, stream);
+}
+
+int rcb_peer_push_bytes(void* const* windows, int32_t n_ranks, int32_t rank, int64_t n_entries,
+                        const void* src_dev, int64_t bytes, uint32_t epoch, void* stream) {
+  if (n_ranks < 1 || n_ranks > rcb::peer::kMaxRanks || rank < 0 || rank >= n_ranks ||
+      n_entries < 1 || windows == nullptr || epoch == 0 || bytes < 8 || bytes % 8 != 0 ||
+      bytes > n_entries * 8 || reinterpret_cast<uintptr_t>(src_dev) % 8 != 0)
+    return set_error(RCB_ERR_ARG, "bad peer byte push arguments");
+  rcb::peer::Windows w{};
+  for (int r = 0; r < n_ranks; ++r) {
+    if (windows[r] == nullptr) return set_error(RCB_ERR_ARG, "missing peer window");
+    w.w[r] = static_cast<uint8_t*>(windows[r]);
+  }
+  rcb::peer::push_bytes_kernel<<<n_ranks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      w, n_ranks, rank, n_entries, static_cast<const long long*>(src_dev), bytes / 8, epoch);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? RCB_OK : set_cuda_error(e, "peer byte push launch");
+}
+
+int rcb_peer_wait(const void* window, int32_t n_ranks, int64_t n_entries, uint32_t epoch,
+                  uint64_t timeout_ns, int32_t* timed_out_dev, void* stream) {
+  if (rcb_peer_window_bytes(n_ranks, n_entries) < 0 || epoch == 0 || timed_out_dev == nullptr)
+    return set_error(RCB_ERR_ARG, "bad peer wait arguments");
+  rcb::peer::wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint8_t*>(window), n_ranks, n_entries, epoch, timeout_ns, timed_out_dev);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? RCB_OK : set_cuda_error(e, "peer wait launch");
+}
+
+int64_t rcb_peer_slot_offset(int32_t n_ranks, int64_t n_entries, uint32_t epoch) {
+  if (rcb_peer_window_bytes(n_ranks, n_entries) < 0) return -1;
+  return rcb::peer::layout(n_ranks, n_entries).ids + int64_t(epoch & 1) * n_ranks * n_entries * 8;
 }
 
 }  // extern "C"

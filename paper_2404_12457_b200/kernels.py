@@ -373,25 +373,44 @@ def topk_merge_shards(ids: torch.Tensor, scores: torch.Tensor, stream=None):
     return ids_out, sc_out
 
 
-class PeerExchange:
-    """Peer-memory exchange of the per-shard staged lists (rcb_peer_*, csrc/peer.cu).
+class _DeviceView:
+    """__cuda_array_interface__ over a raw device range (a view into a peer window)."""
 
-    Each rank allocates an exchange window, exports it as a CUDA IPC handle, all-gathers
-    the handles once (``comm.all_gather_object``) and maps every peer's window (NVLink P2P
-    on one box; the same memory when ranks share a GPU).  ``merge(ids, scores)`` pushes this
-    rank's [n_queries, S, k] lists into slot (epoch & 1, rank) of every window, publishes the
-    epoch, waits for all ranks' epochs and merges its own window: one push + one merge kernel
-    instead of two all-gathers + the merge.  The caller orders successive calls with a
-    collective between them (ShardedRetriever's query all-gather).
+    def __init__(self, ptr: int, shape, typestr: str) -> None:
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+class PeerExchange:
+    """Exchange over peer memory (rcb_peer_*, csrc/peer.cu).
+
+    Each rank allocates an exchange window of ``n_entries`` 8-byte slots per (parity, rank),
+    exports it as a CUDA IPC handle, all-gathers the handles once
+    (``comm.all_gather_object``) and maps every peer's window (NVLink P2P on one box; the
+    same memory when ranks share a GPU).  Two uses:
+
+    * ``merge(ids, scores)`` (``lists=(n_queries, S, k)``): push this rank's staged lists
+      into slot (epoch & 1, rank) of every window, publish the epoch, wait for all ranks'
+      epochs and merge the own window -- one push + one merge kernel instead of two
+      all-gathers + the merge;
+    * ``gather(x)``: a raw all-gather of x's bytes; returns a view of the own window's slot
+      holding every rank's rows in rank order.
+
+    Successive calls of one window alternate parity slots; a rank reuses a slot only two
+    epochs later, after a later exchange of the same step sequence has completed on every
+    rank (ShardedRetriever: queries(e+2) are pushed after lists(e+1) arrived from all ranks,
+    which each rank pushes after scanning queries(e+1), i.e. after it finished with (e)).
     """
 
-    def __init__(self, comm, n_queries: int, n_stages: int, k: int, timeout_s: float = 10.0,
+    def __init__(self, comm, n_entries: int, *, lists=None, timeout_s: float = 10.0,
                  device="cuda") -> None:
         lib = load()
         self.lib = lib
         self.R, self.rank = comm.world, comm.rank
-        self.nq, self.S, self.k = n_queries, n_stages, k
-        self.E = n_queries * n_stages * k
+        self.E = int(n_entries)
+        if lists is not None:
+            self.nq, self.S, self.k = lists
+            assert self.E == self.nq * self.S * self.k
         self.timeout_ns = int(timeout_s * 1e9)
         win = ctypes.c_void_p()
         check(lib.rcb_peer_window_alloc(self.R, self.E, ctypes.byref(win)), "rcb_peer_window_alloc")
@@ -432,10 +451,27 @@ class PeerExchange:
                                       _dev_ptr(ids_out), _dev_ptr(sc_out), st), "rcb_peer_merge")
         return ids_out, sc_out
 
+    def gather(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+        """All-gather of a contiguous device tensor (every rank the same shape, 8E bytes):
+        a [world * x.shape[0], *x.shape[1:]] view of the own window (valid until the slot's
+        next reuse, two calls later)."""
+        nbytes = x.numel() * x.element_size()
+        assert x.is_contiguous() and nbytes == 8 * self.E
+        self.epoch += 1
+        st = _stream(stream)
+        check(self.lib.rcb_peer_push_bytes(self.windows, self.R, self.rank, self.E, _dev_ptr(x),
+                                           nbytes, self.epoch, st), "rcb_peer_push_bytes")
+        check(self.lib.rcb_peer_wait(self.own, self.R, self.E, self.epoch, self.timeout_ns,
+                                     _dev_ptr(self.timed_out), st), "rcb_peer_wait")
+        off = self.lib.rcb_peer_slot_offset(self.R, self.E, self.epoch)
+        words = torch.as_tensor(_DeviceView(self.own + off, (self.R * self.E,), "<i8"),
+                                device=x.device)
+        return words.view(x.dtype).view((self.R * x.shape[0],) + tuple(x.shape[1:]))
+
     def check_timeout(self) -> None:
-        """Raise if any merge gave up waiting for a peer (reads a device flag: syncs)."""
+        """Raise if any wait gave up on a peer (reads a device flag: syncs)."""
         if int(self.timed_out.item()):
-            raise RuntimeError("peer exchange: a rank's lists did not arrive within the timeout")
+            raise RuntimeError("peer exchange: a rank's data did not arrive within the timeout")
 
     def close(self) -> None:
         for p in self.opened:

@@ -81,13 +81,17 @@ class ShardedRetriever:
         self._qpad = torch.zeros((batch, corpus_shard.shape[1]), dtype=torch.bfloat16, device=dev)
         self.launches = 0
         self.bytes_per_scan = corpus_shard.shape[0] * corpus_shard.shape[1] * 2
-        self.px = None
+        self.px = self.pq = None
         self.exchange = "allgather" if self.world == 1 else exchange
         if self.world > 1 and exchange in ("auto", "p2p"):
             if merge is None and dev.type == "cuda":
                 try:
-                    self.px = kernels.PeerExchange(comm, nq, n_stages, k, device=dev)
-                    self.exchange = "p2p"
+                    self.px = kernels.PeerExchange(comm, nq * n_stages * k,
+                                                   lists=(nq, n_stages, k), device=dev)
+                    qbytes = batch * corpus_shard.shape[1] * 2
+                    if qbytes % 8 == 0:  # the queries too: no collective left in the loop
+                        self.pq = kernels.PeerExchange(comm, qbytes // 8, device=dev)
+                    self.exchange = "p2p" if self.pq is not None else "p2p lists"
                 except RuntimeError as exc:  # CUDA IPC / peer mapping unavailable on this box
                     if exchange == "p2p":
                         raise
@@ -124,9 +128,10 @@ class ShardedRetriever:
         if self.world == 1:
             self.scan_all(q_local)
             return (self.ids[:b], self.sc[:b]) if with_scores else self.ids[:b]
-        # the query all-gather also orders successive peer exchanges (every rank has issued
-        # the previous merge before any rank pushes the next lists)
-        allq = self.comm.all_gather(q_local).reshape(-1, q_local.shape[1])
+        if self.pq is not None:  # over peer memory (ordering: kernels.PeerExchange)
+            allq = self.pq.gather(q_local)
+        else:  # the collective also orders successive list exchanges
+            allq = self.comm.all_gather(q_local).reshape(-1, q_local.shape[1])
         self.scan_all(allq)
         if self.px is not None:
             ids, sc = self.px.merge(self.ids, self.sc)

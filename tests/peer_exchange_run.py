@@ -35,10 +35,12 @@ def main():
         same &= bool(torch.equal(i1, i2)) and bool(torch.equal(s1, s2))
     torch.cuda.synchronize()
     p2p.px.check_timeout()
+    p2p.pq.check_timeout()
     print(json.dumps({"rank": d.rank, "exchange": p2p.exchange, "calls": calls,
                       "identical": same, "epoch": p2p.px.epoch}))
     d.barrier()
     p2p.px.close()
+    p2p.pq.close()
     d.close()
 
 

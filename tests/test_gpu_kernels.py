@@ -390,3 +390,42 @@ def test_prefix_prefill_bench_shape_sampled(fused_rope):
         got = out[starts[r]:starts[r] + b].cpu().float()
         err = (got - ref).abs().max().item()
         assert err <= ATTN_ATOL, f"request {r} (alpha {a}, beta {b}): max |err| {err}"
+
+
+# ---------------------------------------------------------------- peer exchange protocol
+@pytest.mark.gpu
+def test_peer_window_epochs_and_bounded_wait():
+    """rcb_peer_* in one process (both 'ranks' map the same window): a wait for an epoch a
+    rank has not published gives up after its timeout and flags it (no device hang); once
+    every rank pushed, the wait passes and the merge sees both ranks' lists in the epoch's
+    parity slot."""
+    import ctypes
+
+    from paper_2404_12457_b200 import _lib
+
+    lib = _lib.load()
+    R, nq, S, k = 2, 3, 2, 2
+    E = nq * S * k
+    win = ctypes.c_void_p()
+    assert lib.rcb_peer_window_alloc(R, E, ctypes.byref(win)) == 0
+    try:
+        wins = (ctypes.c_void_p * R)(win.value, win.value)
+        flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+        ids = [torch.arange(E, device="cuda").view(nq, S, k) * 10 + r for r in range(R)]
+        scs = [torch.full((nq, S, k), float(r), device="cuda") for r in range(R)]
+        assert lib.rcb_peer_push(wins, R, 0, E, ids[0].data_ptr(), scs[0].data_ptr(), 1, None) == 0
+        out_i = torch.empty((nq, S, k), dtype=torch.int64, device="cuda")
+        out_s = torch.empty((nq, S, k), dtype=torch.float32, device="cuda")
+        assert lib.rcb_peer_wait(win.value, R, E, 1, 2_000_000, flag.data_ptr(), None) == 0
+        torch.cuda.synchronize()
+        assert int(flag.item()) == 1  # rank 1 never published epoch 1: bounded, flagged
+        flag.zero_()
+        assert lib.rcb_peer_push(wins, R, 1, E, ids[1].data_ptr(), scs[1].data_ptr(), 1, None) == 0
+        assert lib.rcb_peer_merge(win.value, R, nq, S, k, 1, 2_000_000_000, flag.data_ptr(),
+                                  out_i.data_ptr(), out_s.data_ptr(), None) == 0
+        torch.cuda.synchronize()
+        assert int(flag.item()) == 0
+        # rank 1's scores (1.0) beat rank 0's (0.0): every merged entry comes from rank 1
+        assert torch.all(out_s == 1.0) and torch.all(out_i % 10 == 1)
+    finally:
+        lib.rcb_peer_window_free(win)

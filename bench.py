@@ -42,6 +42,12 @@ sys.path.insert(0, ROOT)
 METRIC = "p50 TTFT (ms) and RAG req/s vs cache hit rate at 1/2/4/8 B200; KV swap GB/s"
 
 
+def WORKLOAD_NAMES():
+    from paper_2404_12457_b200.workloads import WORKLOADS
+
+    return set(WORKLOADS)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -58,6 +64,8 @@ def parse():
                          "batch before the prefill)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ttft", action="store_true")
+    ap.add_argument("--no-hit-sweep", action="store_true",
+                    help="skip the hot-path req/s vs hit rate sweep (part of the ttft block)")
     ap.add_argument("--no-model-step", action="store_true",
                     help="skip timing the bench step's batch through the whole random-init model")
     ap.add_argument("--no-timed", action="store_true",
@@ -193,7 +201,7 @@ def fence_step(dpool, compute, swapped: bool, layers_per_group: int):
     return None
 
 
-def run_ours(args, dist: Dist):
+def run_ours(args, dist: Dist, emit: bool = True):
     from paper_2404_12457_b200 import _lib, synth
     from paper_2404_12457_b200.hotpath import HotPath, StepPlan, apply_events, EventLog, has_swaps
     from paper_2404_12457_b200.pool import accounting_pool
@@ -201,7 +209,8 @@ def run_ours(args, dist: Dist):
     from paper_2404_12457_b200.workloads import pool_blocks
 
     torch.cuda.set_device(0 if args.single_device else dist.local)
-    dist.init(args.backend)
+    if dist.pg is None:  # a hit-rate sweep run reuses the process group
+        dist.init(args.backend)
     dist.device = "cuda"
     w, R, steps, sizes, (lo, hi) = build_workload(args, dist)
     raw_steps = list(steps)  # the planning loop below keeps only each step's admitted prefix
@@ -440,8 +449,40 @@ def run_ours(args, dist: Dist):
             "clocks": clk,
             "cpu_baseline": cpu,
         }
-        print(json.dumps(result))
+        if emit:
+            print(json.dumps(result))
     return result
+
+
+SWEEP_TIERS = (80_000, 200_000, 500_000, 1_100_000)
+
+
+def hit_rate_sweep(args, dist: Dist) -> dict:
+    """The hot-path step's req/s against the cache hit rate (BASELINE metric: "RAG req/s vs
+    cache hit rate"): the repeated-question variant of the workload (ragsim query pool) over
+    GPU tiers from barely above the batch's in-flight need to configs[1]'s, same batch and
+    step, fewer steps; every point a full run_ours (device-timed steps + e2e)."""
+    import copy
+
+    t0 = time.perf_counter()
+    pts = []
+    for tier in SWEEP_TIERS:
+        a = copy.copy(args)
+        a.workload, a.gpu_tier_tokens = args.workload + "-qpool", tier
+        a.no_ttft = a.no_cpu_baseline = a.no_model_step = True
+        a.steps, a.warmup = 5, 3
+        torch.cuda.empty_cache()
+        r = run_ours(a, dist, emit=False)
+        pts.append({"gpu_tier_tokens": tier, "doc_hit_rate": r["doc_hit_rate"],
+                    "req_per_s": r["value"], "e2e_req_per_s": r["e2e"]["value"],
+                    "e2e_doc_hit_rate": r["e2e"]["doc_hit_rate"],
+                    "ms_per_step": r["ms_per_step"], "attention_frac": r["roofline"]["frac"]})
+    return {"workload": args.workload + "-qpool", "batch_per_gpu": r["config"]["batch_per_gpu"],
+            "points": pts, "seconds": round(time.perf_counter() - t0, 1),
+            "how": "each point: bench.py's step (retrieval + KV tiering + K/V write + attention) "
+                   "at that GPU tier, 40 cache-warm + 3 warmup + 5 device-timed steps, e2e "
+                   "through HotPath; hits rise with the tier because the repeated questions' "
+                   "documents stay resident"}
 
 
 def measure_model_step(w, plan, dpool, device, reps: int = 2) -> dict:
@@ -864,7 +905,12 @@ def main():
     if args.impl == "reference":
         run_reference(args, dist)
         return
-    run_ours(args, dist)
+    res = run_ours(args, dist, emit=False)
+    if (res is not None and dist.world == 1 and not args.no_ttft and not args.no_hit_sweep
+            and args.workload + "-qpool" in WORKLOAD_NAMES()):
+        res["hotpath_vs_hit_rate"] = hit_rate_sweep(args, dist)
+    if res is not None:
+        print(json.dumps(res))
     if dist.pg is not None:
         dist.pg.destroy_process_group()
 

@@ -412,27 +412,45 @@ class PeerExchange:
             self.nq, self.S, self.k = lists
             assert self.E == self.nq * self.S * self.k
         self.timeout_ns = int(timeout_s * 1e9)
-        win = ctypes.c_void_p()
-        check(lib.rcb_peer_window_alloc(self.R, self.E, ctypes.byref(win)), "rcb_peer_window_alloc")
-        self.own = win.value
+        self.own = None
         self.opened = []
+        # every rank reaches both agreement rounds whatever fails locally, so the ranks
+        # either all use the windows or all raise (a split decision would deadlock the next
+        # collective against a peer spinning on its window)
+        handle = None
         try:
+            win = ctypes.c_void_p()
+            check(lib.rcb_peer_window_alloc(self.R, self.E, ctypes.byref(win)),
+                  "rcb_peer_window_alloc")
+            self.own = win.value
             h = (ctypes.c_uint8 * _lib.RCB_PEER_HANDLE_BYTES)()
             check(lib.rcb_peer_ipc_handle(self.own, h), "rcb_peer_ipc_handle")
-            handles = comm.all_gather_object(bytes(h))
-            wins = []
-            for r, hb in enumerate(handles):
-                if r == self.rank:
-                    wins.append(self.own)
-                    continue
-                p = ctypes.c_void_p()
-                buf = (ctypes.c_uint8 * len(hb)).from_buffer_copy(hb)
-                check(lib.rcb_peer_open(buf, ctypes.byref(p)), "rcb_peer_open")
-                self.opened.append(p.value)
-                wins.append(p.value)
-        except Exception:
+            handle = bytes(h)
+        except RuntimeError as exc:
+            err = str(exc)
+        handles = comm.all_gather_object(handle)
+        if any(hb is None for hb in handles):
             self.close()
-            raise
+            raise RuntimeError(f"peer window export failed on rank(s) "
+                               f"{[r for r, hb in enumerate(handles) if hb is None]}"
+                               + (f": {err}" if handle is None else ""))
+        wins, ok = [], True
+        for r, hb in enumerate(handles):
+            if r == self.rank:
+                wins.append(self.own)
+                continue
+            p = ctypes.c_void_p()
+            buf = (ctypes.c_uint8 * len(hb)).from_buffer_copy(hb)
+            if lib.rcb_peer_open(buf, ctypes.byref(p)) != 0:
+                ok = False
+                break
+            self.opened.append(p.value)
+            wins.append(p.value)
+        oks = comm.all_gather_object(ok)
+        if not all(oks):
+            self.close()
+            raise RuntimeError(f"peer window mapping failed on rank(s) "
+                               f"{[r for r, o in enumerate(oks) if not o]}")
         self.windows = (ctypes.c_void_p * self.R)(*wins)
         self.epoch = 0
         self.timed_out = torch.zeros(1, dtype=torch.int32, device=device)

@@ -93,6 +93,8 @@ class ShardedRetriever:
                         self.pq = kernels.PeerExchange(comm, qbytes // 8, device=dev)
                     self.exchange = "p2p" if self.pq is not None else "p2p lists"
                 except RuntimeError as exc:  # CUDA IPC / peer mapping unavailable on this box
+                    # (PeerExchange fails on every rank alike, so all ranks fall back together)
+                    self.close()
                     if exchange == "p2p":
                         raise
                     self.exchange = f"allgather (peer exchange unavailable: {exc})"
@@ -110,6 +112,13 @@ class ShardedRetriever:
         kernels.retrieval_topk(self.corpus, q, self.k, self.S, self.off, workspace=self.ws[b - a],
                                ids_out=self.ids[a:b], scores_out=self.sc[a:b])
         self.launches += 2
+
+    def close(self) -> None:
+        """Unmap the peers' exchange windows and free this rank's."""
+        for px in (self.px, self.pq):
+            if px is not None:
+                px.close()
+        self.px = self.pq = None
 
     def scan_all(self, allq: torch.Tensor) -> None:
         """Scan the local shard for a gathered [world*batch, dim] query block."""

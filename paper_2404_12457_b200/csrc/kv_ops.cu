@@ -16,6 +16,10 @@
 #include "rcb_internal.h"
 #include "sm100.cuh"
 
+#ifndef RCB_PDL
+#define RCB_PDL 1
+#endif
+
 namespace rcb {
 
 namespace {
@@ -295,6 +299,11 @@ __global__ void __launch_bounds__(kKvTabThreads)
                              __nv_bfloat16* __restrict__ pool, int block_tokens,
                              int64_t block_elems, int n_kv_heads, int head_dim, int layer,
                              const float4* __restrict__ table) {
+#if RCB_PDL
+  // programmatic dependent launch: the attention launch that follows may start its
+  // prologue on SMs this grid frees (it waits for our writes before reading K/V)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
   const int half = head_dim / 2;
   const int cph = half / 8;  // 16-byte chunks per half row
   const int q_heads = q != nullptr ? n_q_heads : 0;

@@ -48,6 +48,9 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #define RCB_POLY16 2
 #endif
 constexpr int kPoly16 = RCB_POLY16;  // of every 16 columns (even)
+#ifndef RCB_PDL
+#define RCB_PDL 1
+#endif
 
 // TMEM load of one O chunk, 32 or 16 columns (the epilogue's chunk width depends on G)
 __device__ __forceinline__ void tmem_ldn(uint32_t taddr, uint32_t (&r)[32]) { tmem_ld32(taddr, r); }
@@ -284,6 +287,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           ++q_issued;
         }
         const int n = it.n();
+#if RCB_PDL
+        // launched programmatically after the K/V write: Q, tables and the prologue may run
+        // early, the first K/V page load waits for that grid's writes
+        if (ii == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
         for (int j = 0; j < n; ++j, ++s) {
           // next item's Q as soon as its buffer frees (last QK of item ii-1 retired): it
           // then lands (and is rotated) a whole item ahead of its first MMA
@@ -969,10 +977,19 @@ cudaError_t launch_s(const CUtensorMap& tq, const CUtensorMap& tkv, const CUtens
     if (sms <= 0) sms = 148;
   }
   const int grid = n_work < sms ? n_work : sms;
-  kern<<<grid, kThreads, smem, stream>>>(tq, tkv, to, static_cast<__nv_bfloat16*>(out), n_q_heads,
-                                        layer, blk_ids, blk_valid, blk_pos, work, n_work,
-                                        scale_log2, rope, part_o, part_ml);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = RCB_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tq, tkv, to, static_cast<__nv_bfloat16*>(out), n_q_heads,
+                            layer, blk_ids, blk_valid, blk_pos, work, n_work, scale_log2, rope,
+                            part_o, part_ml);
 }
 
 template <int HD, int G, int BT>

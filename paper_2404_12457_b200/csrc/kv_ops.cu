@@ -288,6 +288,10 @@ __global__ void __launch_bounds__(kRopeThreads)
 constexpr int kKvTok = RCB_KV_TOK;
 constexpr int kKvUnroll = RCB_KV_UNROLL;
 constexpr int kKvTabThreads = 256;
+#ifndef RCB_KV_V32
+#define RCB_KV_V32 1
+#endif
+constexpr bool kKvV32 = RCB_KV_V32 != 0;
 
 __global__ void __launch_bounds__(kKvTabThreads)
     kv_write_rope_tab_kernel(const __nv_bfloat16* __restrict__ q, int64_t q_stride,
@@ -308,7 +312,11 @@ __global__ void __launch_bounds__(kKvTabThreads)
   const int cph = half / 8;  // 16-byte chunks per half row
   const int q_heads = q != nullptr ? n_q_heads : 0;
   const int rot_units = (q_heads + n_kv_heads) * cph;
-  const int per_tok = rot_units + n_kv_heads * (head_dim / 8);
+  // V moves in 32-byte chunks when rows allow (half the memory instructions of 16-byte ones)
+  const int vw = (kKvV32 && kv_stride % 16 == 0 && head_dim % 16 == 0 &&
+                  (reinterpret_cast<uintptr_t>(v) & 31) == 0 &&
+                  (reinterpret_cast<uintptr_t>(pool) & 31) == 0) ? 16 : 8;
+  const int per_tok = rot_units + n_kv_heads * (head_dim / vw);
   const int t0 = blockIdx.x * kKvTok;
   const int n = min(kKvTok, n_tokens - t0) * per_tok;
   const int64_t tile = int64_t(block_tokens) * head_dim;
@@ -359,10 +367,23 @@ __global__ void __launch_bounds__(kKvTabThreads)
       *reinterpret_cast<uint4*>(dst + c + half) = pack8(y1);
     } else {
       const int jj = j - rot_units;
-      const int h = jj / (head_dim / 8);
-      const int c = (jj - h * (head_dim / 8)) * 8;
-      *reinterpret_cast<uint4*>(kbase + int64_t(n_kv_heads + h) * tile + c) =
-          *reinterpret_cast<const uint4*>(v + int64_t(t) * kv_stride + int64_t(h) * head_dim + c);
+      const int h = jj / (head_dim / vw);
+      const int c = (jj - h * (head_dim / vw)) * vw;
+      const __nv_bfloat16* vs = v + int64_t(t) * kv_stride + int64_t(h) * head_dim + c;
+      __nv_bfloat16* vd = kbase + int64_t(n_kv_heads + h) * tile + c;
+      if (vw == 16) {
+        uint4 lo, hi;
+        asm volatile("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y),
+                       "=r"(hi.z), "=r"(hi.w)
+                     : "l"(vs));
+        asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(vd),
+                     "r"(lo.x), "r"(lo.y), "r"(lo.z), "r"(lo.w), "r"(hi.x), "r"(hi.y), "r"(hi.z),
+                     "r"(hi.w)
+                     : "memory");
+      } else {
+        *reinterpret_cast<uint4*>(vd) = *reinterpret_cast<const uint4*>(vs);
+      }
     }
   }
 }

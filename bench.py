@@ -484,12 +484,19 @@ def hit_rate_sweep(args, dist: Dist) -> dict:
         a.no_ttft = a.no_cpu_baseline = a.no_model_step = True
         a.steps, a.warmup = 5, 3
         torch.cuda.empty_cache()
-        r = run_ours(a, dist, emit=False)
+        try:
+            r = run_ours(a, dist, emit=False)
+        except Exception as exc:  # noqa: BLE001 - a failed point must not lose the main line
+            pts.append({"gpu_tier_tokens": tier, "error": f"{type(exc).__name__}: {exc}"[:300]})
+            continue
         pts.append({"gpu_tier_tokens": tier, "doc_hit_rate": r["doc_hit_rate"],
                     "req_per_s": r["value"], "e2e_req_per_s": r["e2e"]["value"],
                     "e2e_doc_hit_rate": r["e2e"]["doc_hit_rate"],
                     "ms_per_step": r["ms_per_step"], "attention_frac": r["roofline"]["frac"]})
-    return {"workload": args.workload + "-qpool", "batch_per_gpu": r["config"]["batch_per_gpu"],
+    from paper_2404_12457_b200.workloads import WORKLOADS
+
+    return {"workload": args.workload + "-qpool",
+            "batch_per_gpu": args.batch or WORKLOADS[args.workload + "-qpool"].batch,
             "points": pts, "seconds": round(time.perf_counter() - t0, 1),
             "how": "each point: bench.py's step (retrieval + KV tiering + K/V write + attention) "
                    "at that GPU tier, 40 cache-warm + 3 warmup + 5 device-timed steps, e2e "

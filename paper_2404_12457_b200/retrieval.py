@@ -138,7 +138,7 @@ class ShardedRetriever:
             self.scan_all(q_local)
             return (self.ids[:b], self.sc[:b]) if with_scores else self.ids[:b]
         if self.pq is not None:  # over peer memory (ordering: kernels.PeerExchange)
-            allq = self.pq.gather(q_local)
+            allq = self.pq.gather(q_local.contiguous())
         else:  # the collective also orders successive list exchanges
             allq = self.comm.all_gather(q_local).reshape(-1, q_local.shape[1])
         self.scan_all(allq)

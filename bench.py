@@ -159,6 +159,16 @@ def peaks():
         return 6650.0, 1400.0, "fallback (B200_PROFILING.md)"
 
 
+def guarded(fn, *a, **kw):
+    """A side measurement (model step, TTFT curves) that fails records the error in its
+    block instead of losing the bench line."""
+    try:
+        return fn(*a, **kw)
+    except Exception as exc:  # noqa: BLE001
+        torch.cuda.empty_cache()
+        return {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
+
 def burst_frac(achieved_tf: float, clk: dict):
     try:
         p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -380,7 +390,7 @@ def run_ours(args, dist: Dist, emit: bool = True):
         (st1["kernel_launches"] - st0["kernel_launches"])
 
     # ---- the same step with the model around the hot path (paper-sense prefill req/s)
-    model_step = (measure_model_step(w, plans[W], dpool, device)
+    model_step = (guarded(measure_model_step, w, plans[W], dpool, device)
                   if dist.rank == 0 and not args.no_model_step else None)
 
     # ---- e2e: live steps through the public API (host buffers, host decisions)
@@ -393,8 +403,9 @@ def run_ours(args, dist: Dist, emit: bool = True):
     if dist.rank == 0 and not args.no_ttft:
         del corpus, retr, qkv, q_rot, out
         torch.cuda.empty_cache()
-        ttft = measure_ttft(w, swap, stage_ms=(sum(scan_ms) / max(1, len(scan_ms))) / w.n_stages,
-                            timed_on=not args.no_timed)
+        ttft = guarded(measure_ttft, w, swap,
+                       stage_ms=(sum(scan_ms) / max(1, len(scan_ms))) / w.n_stages,
+                       timed_on=not args.no_timed)
 
     result = None
     if dist.rank == 0:

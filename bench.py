@@ -938,7 +938,7 @@ def main():
     res = run_ours(args, dist, emit=False)
     if (res is not None and dist.world == 1 and not args.no_ttft and not args.no_hit_sweep
             and args.workload + "-qpool" in WORKLOAD_NAMES()):
-        res["hotpath_vs_hit_rate"] = hit_rate_sweep(args, dist)
+        res["hotpath_vs_hit_rate"] = guarded(hit_rate_sweep, args, dist)
     if res is not None:
         print(json.dumps(res))
     if dist.pg is not None:

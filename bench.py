@@ -392,6 +392,7 @@ def run_ours(args, dist: Dist, emit: bool = True):
     # ---- the same step with the model around the hot path (paper-sense prefill req/s)
     model_step = (guarded(measure_model_step, w, plans[W], dpool, device)
                   if dist.rank == 0 and not args.no_model_step else None)
+    dist.barrier()  # the other ranks wait on the host, not in a peer-exchange spin
 
     # ---- e2e: live steps through the public API (host buffers, host decisions)
     e2e = run_e2e(args, dist, w, R, steps, planner, device, dpool, retr, qkv, q_rot, out,

@@ -101,15 +101,18 @@ def test_cached_prefix_logits_at_bench_geometry(model):
     assert max(errs) <= LOGIT_ATOL, f"{model}: max |logit err| per request {errs} (max |logit| {mag:.3f})"
 
 
-def test_whole_bench_step_attention_against_fp32():
-    """configs[1]'s step: the planner's admissions after the bench's cache warm-up."""
+@pytest.mark.parametrize("workload,R", [("mistral7b-100k", 64), ("llama2-13b-10m", 32)])
+def test_whole_bench_step_attention_against_fp32(workload, R):
+    """A bench step (configs[1]: GQA-4, staged O stores; configs[3]: MHA with 40 heads, direct
+    O stores and the 16-column drain): the planner's admissions after the bench's cache
+    warm-up, one fused-RoPE launch, every request against the fp32 oracle."""
     from paper_2404_12457_b200.hotpath import HotPath  # puts ragsim on the path
     from paper_2404_12457_b200.pool import accounting_pool
     from paper_2404_12457_b200.workloads import WORKLOADS, make_stream, pool_blocks
     from ragsim.cost_model import synthetic_profile
 
-    w = WORKLOADS["mistral7b-100k"]
-    R, n_warm = 64, 40
+    w = WORKLOADS[workload]
+    n_warm = 40
     trace, sizes = make_stream(w, (n_warm + 1) * R)
     ng = pool_blocks(w.gpu_capacity_tokens, w.block_tokens, sizes.values(), R * (w.k + 1))
     hp = HotPath(w.model, gpu_capacity_tokens=w.gpu_capacity_tokens, host_capacity_tokens=0,
@@ -123,7 +126,8 @@ def test_whole_bench_step_attention_against_fp32():
         if i < n_warm:
             for a in adm:
                 hp.commit(a)
-    assert len(adm) == R and any(a.alpha > 0 for a in adm) and any(a.alpha == 0 for a in adm)
+    assert len(adm) == R and any(a.alpha == 0 for a in adm)
+    assert any(a.alpha > 0 for a in adm) or workload != "mistral7b-100k"
     # one layer of the step's pages, block ids remapped onto a compact pool
     s = w.model
     used = sorted({b for a in adm for b in a.blocks})

@@ -288,6 +288,10 @@ __global__ void __launch_bounds__(kRopeThreads)
 constexpr int kKvTok = RCB_KV_TOK;
 constexpr int kKvUnroll = RCB_KV_UNROLL;
 constexpr int kKvTabThreads = 256;
+#ifndef RCB_KV_UNITS
+#define RCB_KV_UNITS 1024
+#endif
+constexpr int kKvTabUnits = RCB_KV_UNITS;  // chunk units per CTA the token count aims at
 #ifndef RCB_KV_V32
 #define RCB_KV_V32 1
 #endif
@@ -302,7 +306,7 @@ __global__ void __launch_bounds__(kKvTabThreads)
                              const int32_t* __restrict__ slots, int n_tokens, int n_q_heads,
                              __nv_bfloat16* __restrict__ pool, int block_tokens,
                              int64_t block_elems, int n_kv_heads, int head_dim, int layer,
-                             const float4* __restrict__ table) {
+                             const float4* __restrict__ table, int tok_per_cta) {
 #if RCB_PDL
   // programmatic dependent launch: the attention launch that follows may start its
   // prologue on SMs this grid frees (it waits for our writes before reading K/V)
@@ -317,8 +321,8 @@ __global__ void __launch_bounds__(kKvTabThreads)
                   (reinterpret_cast<uintptr_t>(v) & 31) == 0 &&
                   (reinterpret_cast<uintptr_t>(pool) & 31) == 0) ? 16 : 8;
   const int per_tok = rot_units + n_kv_heads * (head_dim / vw);
-  const int t0 = blockIdx.x * kKvTok;
-  const int n = min(kKvTok, n_tokens - t0) * per_tok;
+  const int t0 = blockIdx.x * tok_per_cta;
+  const int n = min(tok_per_cta, n_tokens - t0) * per_tok;
   const int64_t tile = int64_t(block_tokens) * head_dim;
 #pragma unroll kKvUnroll
   for (int u = threadIdx.x; u < n; u += kKvTabThreads) {
@@ -519,13 +523,18 @@ extern "C" int rcb_kv_write_rope_table(const void* q, int64_t q_stride, const vo
     return rcb::set_error(RCB_ERR_ARG, "q/kv row strides must be multiples of 8 elements");
   if (rope_table_dev == nullptr) return rcb::set_error(RCB_ERR_ARG, "rope table required");
   const int64_t block_elems = int64_t(n_layers) * 2 * n_kv_heads * block_tokens * head_dim;
-  const int grid = (n_tokens + rcb::kKvTok - 1) / rcb::kKvTok;
+  // tokens per CTA: kKvTok at GQA widths (Mistral-7B: 128 chunk units per token, 4 per
+  // thread); wide MHA rows (LLaMA2: 512-640 units per token) take fewer tokens per CTA so
+  // each thread keeps ~4 units and the grid spans more waves
+  const int per_tok = ((q != nullptr ? n_q_heads : 0) + 2 * n_kv_heads) * (head_dim / 16);
+  const int tpc = std::max(1, std::min(rcb::kKvTok, rcb::kKvTabUnits / per_tok));
+  const int grid = (n_tokens + tpc - 1) / tpc;
   rcb::kv_write_rope_tab_kernel<<<grid, rcb::kKvTabThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const __nv_bfloat16*>(q), q_stride, static_cast<const __nv_bfloat16*>(k),
       static_cast<const __nv_bfloat16*>(v), kv_stride, static_cast<__nv_bfloat16*>(q_out),
       positions_dev, slots_dev, n_tokens, n_q_heads, static_cast<__nv_bfloat16*>(kv_pool),
       block_tokens, block_elems, n_kv_heads, head_dim, layer,
-      static_cast<const float4*>(rope_table_dev));
+      static_cast<const float4*>(rope_table_dev), tpc);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return rcb::set_cuda_error(e, "rcb_kv_write_rope_table");
   return RCB_OK;

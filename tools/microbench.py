@@ -264,6 +264,7 @@ def bench_attn():
         v = x[:, (hq + hkv) * hd:]
         qr = torch.empty((T, hq, hd), dtype=torch.bfloat16, device="cuda")
         for mode, qq, qo, tab in (("qkv", x[:, : hq * hd], qr, None),
+                                  ("qkv_table", x[:, : hq * hd], qr, rope),
                                   ("kv_only", None, None, None),
                                   ("kv_only_table", None, None, rope)):
             mp = int(pos_t.max()) + 1  # outside the timed call (a device sync)

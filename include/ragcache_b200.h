@@ -181,12 +181,6 @@ int rcb_rope_table(void* table_dev, int32_t max_pos, int32_t head_dim, float rop
  *                 combine_dev = int32 [n_combine][6] {q_start, q_len, tok_base, kv_head,
  *                 slot0, n_parts} merges them into o.  NULL / 0 when unused. */
 #define RCB_WORK_SPLIT_ONLY 1
-/* RCB_WORK_DYNAMIC: CTAs fetch items from an atomic counter instead of the static
- * c, c + grid, ... assignment (set by the planner when the static split is imbalanced);
- * work_dev must then be followed by 4 int32 words that are zero before the first launch
- * (the kernel leaves them zero after each launch; launches sharing one work list must be
- * stream-ordered) */
-#define RCB_WORK_DYNAMIC 2
 int rcb_prefix_prefill(const void* q, int64_t q_row_stride, void* o, int32_t total_q_tokens,
                        int32_t n_q_heads, const void* kv_pool, int64_t num_pool_blocks,
                        int32_t block_tokens, int32_t n_layers, int32_t n_kv_heads,

@@ -34,7 +34,6 @@ RCB_SWAP_DMA = 2
 RCB_POOL_ACCOUNTING = 3
 
 RCB_WORK_SPLIT_ONLY = 1
-RCB_WORK_DYNAMIC = 2
 
 
 class RcbUnavailable(RuntimeError):

@@ -79,8 +79,6 @@ __device__ long long g_trace[kTraceTiles * kTraceEv];
   } while (0)
 #endif
 
-constexpr int kIdxSlots = 16;  // item-index ring of the dynamic work fetch (RCB_DYN)
-
 // barrier indices (pairs indexed by item parity or by query tile w)
 // P handoff per 64-key half: kPFull0 = P columns of keys [0, 64), kPFullB0 = keys [64, 128)
 // (arrived for every tile, right after kPFull0 on a half tile); kPVDone0 = PV of the first
@@ -112,11 +110,8 @@ struct Smem {
   static constexpr uint32_t offL = offMeta + kMetaSlots * 2 * kBPT * 4;  // float2 [2][128]
   static constexpr uint32_t offBar = offL + 2 * 128 * 8;
   static constexpr int kNumBars = kKVFull0 + 2 * kStages;
-  static constexpr int kIdxBar0 = kNumBars;  // [kIdxSlots] item-index ring (dynamic fetch)
-  static constexpr uint32_t offIdx = offBar + (kNumBars + kIdxSlots) * 8;  // int [kIdxSlots]
   // the dynamic window starts 1024-aligned (checked at kernel entry): no slack
-  static constexpr uint32_t kTotal = offIdx + kIdxSlots * 4 + 16;
-  static_assert(kTotal <= 232448, "shared memory per CTA");
+  static constexpr uint32_t kTotal = offBar + kNumBars * 8 + 16;
 };
 
 // Work items are self-contained (no dependent loads at item start):
@@ -136,12 +131,6 @@ struct Smem {
 // epilogue's arrival on Q_empty then releases the buffer for Q(ii + 2).  Ragged tiles and
 // split-KV parts keep the per-lane stores, and so do G <= 2 launches (kStageO below).
 constexpr bool kOTma = RCB_OTMA != 0;
-// Dynamic work fetch (RCB_WORK_DYNAMIC plans): a CTA's first item is blockIdx.x, every
-// further item comes from an atomic counter (the 4 int32 words after the work list; zero
-// before a launch, reset by the last CTA to finish).  The producer fetches two items ahead
-// and publishes each index in an smem ring (kIdxSlots slots, one mbarrier each) that the
-// MMA, softmax and epilogue roles read in the same order; index -1 ends the sequence.
-// Static plans: CTA c serves items c, c + grid, ...
 constexpr int kItemInts = 8;
 struct Item {
   int q_start, q_len, q_pos0, blk_begin, blk_count, qp, kvh, n0, n1;
@@ -193,10 +182,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                           const int* __restrict__ blk_ids, const int* __restrict__ blk_valid,
                           const int* __restrict__ blk_pos, const int* __restrict__ work,
                           int n_work, float scale_log2, const float2* __restrict__ rope,
-                          float* __restrict__ part_o, float2* __restrict__ part_ml,
-                          int dyn_fetch) {
+                          float* __restrict__ part_o, float2* __restrict__ part_ml) {
   using S = Smem<HD, BT, SPLIT>;
-  const bool dyn = dyn_fetch != 0;
   constexpr int TQ = kRows / G;  // tokens per query tile
   // O through the Q buffer + TMA store for G > 2 only.  Q(ii + 2) then lands only after item
   // ii's O left the buffer, and with fused RoPE it must still be rotated before item ii + 2
@@ -222,19 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::offBar);
   uint64_t* kv_full = bar + kKVFull0;
   uint64_t* kv_empty = bar + kKVFull0 + NS;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::offIdx + kIdxSlots * 4);
-  int* sIdx = reinterpret_cast<int*>(smem + S::offIdx);
-  uint64_t* idx_full = bar + S::kIdxBar0;
-  int* sched = const_cast<int*>(work) + n_work * kItemInts;  // dynamic fetch counter + done
-  // item index of this CTA's ii-th item (-1: none); static: blockIdx.x + ii * gridDim.x
-  auto item_idx = [&](int ii) -> int {
-    if (!dyn) {
-      const int idx = (int)blockIdx.x + ii * (int)gridDim.x;
-      return idx < n_work ? idx : -1;
-    }
-    mbar_wait(&idx_full[ii % kIdxSlots], (ii / kIdxSlots) & 1);
-    return sIdx[ii % kIdxSlots];
-  };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + S::kNumBars);
 
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
@@ -259,7 +234,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&kv_full[b], 1);
       mbar_init(&kv_empty[b], 1);
     }
-    for (int b = 0; b < kIdxSlots; ++b) mbar_init(&idx_full[b], 1);
     fence_barrier_init();
   }
   if (warp == 5) tmem_alloc<512>(tmem_slot);
@@ -305,21 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_5d(sKV + st * S::kKV + h * 16384 + b * BT * 128, &tm_kv, &kv_full[st],
                         h * 64, 0, kvh, 2 * layer + kv, ids[b]);
       };
-      auto publish = [&](int ii, int idx) {
-        sIdx[ii % kIdxSlots] = idx;
-        mbar_arrive(&idx_full[ii % kIdxSlots]);  // release: publishes sIdx[slot]
-      };
-      auto fetch = [&]() -> int {
-        const int g = (int)gridDim.x + atomicAdd(sched, 1);
-        return g < n_work ? g : -1;
-      };
-      int nxt = -1, nxt2 = -1;  // indices of items ii + 1, ii + 2 (dynamic fetch)
-      if (dyn) {
-        publish(0, blockIdx.x);  // the grid never exceeds n_work
-        nxt = fetch();
-      }
-      for (int idx = blockIdx.x, ii = 0; idx >= 0; ++ii) {
-        if (!dyn) nxt = idx + (int)gridDim.x < n_work ? idx + (int)gridDim.x : -1;
+      for (int idx = blockIdx.x, ii = 0; idx < n_work; idx += gridDim.x, ++ii) {
         const Item it = load_item(work, idx);
         if (q_issued == ii) {
           mbar_wait(&bar[kQEmpty0 + (ii & 1)], ((ii >> 1) & 1) ^ 1);
@@ -334,12 +294,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
         for (int j = 0; j < n; ++j, ++s) {
           // next item's Q as soon as its buffer frees (last QK of item ii-1 retired): it
-          // then lands (and is rotated) a whole item ahead of its first MMA.  Dynamic fetch:
-          // item ii + 1's index is published after the first K/V step of item ii is issued
-          // (the atomic behind it was issued an item earlier), so it is known from j = 1
-          if ((!dyn || j > 0) && q_issued == ii + 1 && nxt >= 0 &&
+          // then lands (and is rotated) a whole item ahead of its first MMA
+          if (q_issued == ii + 1 && idx + (int)gridDim.x < n_work &&
               mbar_test(&bar[kQEmpty0 + ((ii + 1) & 1)], (((ii + 1) >> 1) & 1) ^ 1)) {
-            issue_q(nxt, ii + 1);
+            issue_q(idx + gridDim.x, ii + 1);
             ++q_issued;
           }
           int ids[BPT];
@@ -370,13 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive(&bar[kMetaFull0 + ms]);  // release: publishes sMeta[ms]
           load_kv(2 * s + 1, 1, ids, it.kvh);
           TRACE(s, 18);
-          if (dyn && j == 0) {
-            nxt2 = nxt >= 0 ? fetch() : -1;  // its result is first used one item later
-            publish(ii + 1, nxt);
-          }
         }
-        idx = nxt;
-        if (dyn) nxt = nxt2;
       }
     }
   } else if (warp == 5) {
@@ -444,9 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit(&bar[kSFull0 + w]);
         ++c[w];
       };
-      for (int ii = 0;; ++ii) {
-        const int idx = item_idx(ii);
-        if (idx < 0) break;
+      for (int idx = blockIdx.x, ii = 0; idx < n_work; idx += gridDim.x, ++ii) {
         const Item it = load_item(work, idx);
         const int n = it.n();
         const int qb = ii & 1;
@@ -543,9 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // phase already, the others consume it after the next S-full (free: that PV precedes
     // the next QK_w in MMA order) or at exit, so every arrival is waited (synccheck)
     bool pv_pending = false;
-    for (int ii = 0;; ++ii) {
-      const int idx = item_idx(ii);
-      if (idx < 0) break;
+    for (int idx = blockIdx.x; idx < n_work; idx += gridDim.x) {
       const Item it = load_item(work, idx);
       const int n = it.n();
       const int tok = (2 * it.qp + it.qtile(wg)) * TQ + t_local;
@@ -927,16 +875,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (use0) ++oc[0];
       if (use1) ++oc[1];
     };
+    const int n_mine =
+        n_work > (int)blockIdx.x ? (n_work - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    auto item_of = [&](int ii) { return load_item(work, blockIdx.x + ii * gridDim.x); };
     // O_w is single-buffered, so item ii's epilogue must finish before item ii+1's first
     // PV_w and runs first; with a RoPE table, Q(ii+2) is rotated next (Q is double
     // buffered: it lands once the last QK of item ii retired; needed by item ii+2).
-    // id0, id1, id2: indices of items ii, ii + 1, ii + 2 (none is waited for past a -1)
-    int id0 = item_idx(0);
-    if (rope != nullptr && id0 >= 0) rotate_q(load_item(work, id0), 0);
-    int id1 = id0 >= 0 ? item_idx(1) : -1;  // published once item 0's first K/V step is issued
-    if (rope != nullptr && id1 >= 0) rotate_q(load_item(work, id1), 1);
-    for (int ii = 0; id0 >= 0; ++ii) {
-      const Item it = load_item(work, id0);
+    constexpr int kAhead = 2;
+    if (rope != nullptr)
+      for (int ii = 0; ii < kAhead && ii < n_mine; ++ii) rotate_q(item_of(ii), ii);
+    for (int ii = 0; ii < n_mine; ++ii) {
+      const Item it = item_of(ii);
       if (it.split()) {
         epilogue(it, 0, true, it.has(1), ii & 1, ii);
       } else {
@@ -947,10 +896,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_store_wait_read();
         mbar_arrive(&bar[kQEmpty0 + (ii & 1)]);
       }
-      const int id2 = id1 >= 0 ? item_idx(ii + 2) : -1;
-      if (rope != nullptr && id2 >= 0) rotate_q(load_item(work, id2), ii + 2);
-      id0 = id1;
-      id1 = id2;
+      if (rope != nullptr && ii + kAhead < n_mine) rotate_q(item_of(ii + kAhead), ii + kAhead);
     }
     if (kStageO && row == 0) tma_store_wait_all();
     tc_fence_before();
@@ -959,15 +905,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 5) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
-  }
-  if (dyn && threadIdx.x == 0) {
-    // every fetch of this CTA precedes the barrier above; the last CTA to get here resets
-    // the counter for the next launch on this work list (stream order)
-    __threadfence();
-    if (atomicAdd(sched + 1, 1) == (int)gridDim.x - 1) {
-      atomicExch(sched, 0);
-      atomicExch(sched + 1, 0);
-    }
   }
 }
 
@@ -1023,8 +960,7 @@ template <int HD, int G, int BT, bool SPLIT>
 cudaError_t launch_s(const CUtensorMap& tq, const CUtensorMap& tkv, const CUtensorMap& to, void* out, int n_q_heads,
                      int layer, const int* blk_ids, const int* blk_valid,
                      const int* blk_pos, const int* work, int n_work, float scale_log2,
-                     const float2* rope, float* part_o, float2* part_ml, cudaStream_t stream,
-                     int dyn) {
+                     const float2* rope, float* part_o, float2* part_ml, cudaStream_t stream) {
   auto kern = prefix_prefill_kernel<HD, G, BT, SPLIT>;
   const uint32_t smem = Smem<HD, BT, SPLIT>::kTotal;
   static bool attr_set = false;  // per instantiation
@@ -1053,28 +989,28 @@ cudaError_t launch_s(const CUtensorMap& tq, const CUtensorMap& tkv, const CUtens
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, tq, tkv, to, static_cast<__nv_bfloat16*>(out), n_q_heads,
                             layer, blk_ids, blk_valid, blk_pos, work, n_work, scale_log2, rope,
-                            part_o, part_ml, dyn);
+                            part_o, part_ml);
 }
 
 template <int HD, int G, int BT>
 cudaError_t launch_t(bool split, const CUtensorMap& tq, const CUtensorMap& tkv, const CUtensorMap& to, void* out,
                      int n_q_heads, int layer, const int* bi, const int* bv, const int* bp,
                      const int* work, int n_work, float sl2, const float2* rope,
-                     float* po, float2* pm, cudaStream_t st, int dyn) {
-  return split ? launch_s<HD, G, BT, true>(tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st, dyn)
-               : launch_s<HD, G, BT, false>(tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st, dyn);
+                     float* po, float2* pm, cudaStream_t st) {
+  return split ? launch_s<HD, G, BT, true>(tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st)
+               : launch_s<HD, G, BT, false>(tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
 }
 
 template <int HD, int G>
 cudaError_t launch_bt(bool split, int bt, const CUtensorMap& tq, const CUtensorMap& tkv, const CUtensorMap& to, void* out,
                       int n_q_heads, int layer, const int* bi, const int* bv,
                       const int* bp, const int* work, int n_work, float sl2, const float2* rope,
-                      float* po, float2* pm, cudaStream_t st, int dyn) {
+                      float* po, float2* pm, cudaStream_t st) {
   switch (bt) {
-    case 16: return launch_t<HD, G, 16>(split, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st, dyn);
-    case 32: return launch_t<HD, G, 32>(split, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st, dyn);
-    case 64: return launch_t<HD, G, 64>(split, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st, dyn);
-    case 128: return launch_t<HD, G, 128>(split, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st, dyn);
+    case 16: return launch_t<HD, G, 16>(split, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
+    case 32: return launch_t<HD, G, 32>(split, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
+    case 64: return launch_t<HD, G, 64>(split, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
+    case 128: return launch_t<HD, G, 128>(split, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -1083,12 +1019,12 @@ template <int HD>
 cudaError_t launch_g(bool split, int g, int bt, const CUtensorMap& tq, const CUtensorMap& tkv, const CUtensorMap& to, void* out,
                      int n_q_heads, int layer, const int* bi, const int* bv,
                      const int* bp, const int* work, int n_work, float sl2, const float2* rope,
-                     float* po, float2* pm, cudaStream_t st, int dyn) {
+                     float* po, float2* pm, cudaStream_t st) {
   switch (g) {
-    case 1: return launch_bt<HD, 1>(split, bt, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st, dyn);
-    case 2: return launch_bt<HD, 2>(split, bt, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st, dyn);
-    case 4: return launch_bt<HD, 4>(split, bt, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st, dyn);
-    case 8: return launch_bt<HD, 8>(split, bt, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st, dyn);
+    case 1: return launch_bt<HD, 1>(split, bt, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
+    case 2: return launch_bt<HD, 2>(split, bt, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
+    case 4: return launch_bt<HD, 4>(split, bt, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
+    case 8: return launch_bt<HD, 8>(split, bt, tq, tkv, to, out, n_q_heads, layer, bi, bv, bp, work, n_work, sl2, rope, po, pm, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -1106,8 +1042,6 @@ int prefix_prefill(const void* q, int64_t q_row_stride, void* o, int total_q_tok
   if (reinterpret_cast<uintptr_t>(o) % 32 != 0)
     return set_error(RCB_ERR_ARG, "attention output must be 32-byte aligned");
   const bool split_only = (work_flags & RCB_WORK_SPLIT_ONLY) != 0;
-  // dynamic work fetch: the 4 words after the work list are the kernel's counter
-  const int dyn = (work_flags & RCB_WORK_DYNAMIC) != 0;
   if (n_combine > 0 && (!split_only || part_ws == nullptr || combine == nullptr || n_part_slots <= 0))
     return set_error(RCB_ERR_ARG, "split-KV parts need a split-only plan and a part workspace");
   // part workspace: float2 (max, sum) [slots][128 rows], then fp32 O [slots][128 rows][head_dim]
@@ -1153,10 +1087,10 @@ int prefix_prefill(const void* q, int64_t q_row_stride, void* o, int total_q_tok
       head_dim == 128
           ? attn::launch_g<128>(split_only, g, block_tokens, tq, tkv, to, o, n_q_heads, layer, blk_ids,
                                 blk_valid, blk_pos, work, n_work, sl2,
-                                static_cast<const float2*>(rope_table), part_o, part_ml, stream, dyn)
+                                static_cast<const float2*>(rope_table), part_o, part_ml, stream)
           : attn::launch_g<64>(split_only, g, block_tokens, tq, tkv, to, o, n_q_heads, layer, blk_ids,
                                blk_valid, blk_pos, work, n_work, sl2,
-                               static_cast<const float2*>(rope_table), part_o, part_ml, stream, dyn);
+                               static_cast<const float2*>(rope_table), part_o, part_ml, stream);
   if (e != cudaSuccess) return set_cuda_error(e, "prefix_prefill launch");
   if (n_combine > 0) {
     attn::attn_combine_kernel<<<n_combine, attn::kRows, 0, stream>>>(

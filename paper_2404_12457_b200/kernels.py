@@ -185,8 +185,7 @@ class AttnPlan:
     """
 
     def __init__(self, requests, *, block_tokens: int, n_q_heads: int, n_kv_heads: int,
-                 device="cuda", split_kv: bool | None = None,
-                 dynamic: bool | None = None) -> None:
+                 device="cuda", split_kv: bool | None = None) -> None:
         meta = []
         ids: list[int] = []
         valid: list[int] = []
@@ -233,38 +232,22 @@ class AttnPlan:
         # variant with one Q tile per item buffer and a deeper K/V ring
         self.work_flags = _lib.RCB_WORK_SPLIT_ONLY if not self.tiles_q1.any() else 0
         self.mma_tiles = int((self.tiles_q0 + self.tiles_q1).sum()) if self.n_work else 0
-        # dynamic work fetch when the static c, c + grid, ... split is imbalanced and there are
-        # enough items per CTA for greedy fetching to even it out (modelled cost per item: its
-        # KV steps + 0.3 for the boundary).  Measured (r2m): mixed bench step +1.1% with it;
-        # launches with few items per CTA or equal items only pay the fetch overhead
-        # (single-request launches +8%, MHA miss batch +3%), so they stay static
-        self.dynamic = bool(dynamic) and self.n_work > 0 and not self.work_flags
-        if dynamic is None and os.environ.get("RCB_DYNAMIC", "1") != "0" and self.n_work \
-                and not self.work_flags:
-            grid = min(self.n_work, _num_sms(device))
-            if self.n_work >= 16 * grid:
-                cost = np.maximum(self.tiles_q0, self.tiles_q1) + 0.3
-                loads = np.bincount(np.arange(self.n_work) % grid, weights=cost, minlength=grid)
-                self.dynamic = bool(loads.max() >= 1.04 * loads.mean())
-        if self.dynamic:
-            self.work_flags |= _lib.RCB_WORK_DYNAMIC
         items = work[: self.n_work * 8].reshape(-1, 8)
         groups = np.zeros((0, 6), dtype=np.int32)
         self.n_part_slots = 0
         if split_kv is None:  # opt-in: measured slower at the sizes it targets
             split_kv = bool(os.environ.get("RCB_SPLIT_KV"))
-        if split_kv and self.work_flags & _lib.RCB_WORK_SPLIT_ONLY and 0 < self.n_work and 2 * self.n_work <= _num_sms(device):
+        if split_kv and self.work_flags and 0 < self.n_work and 2 * self.n_work <= _num_sms(device):
             items, groups = _split_kv(items, _num_sms(device), 128 // block_tokens, 128 // g)
             self.n_part_slots = int(groups[:, 5].sum()) if len(groups) else 0
         self.n_work = items.shape[0]
         self.n_combine = groups.shape[0]
-        # work items first: the kernel reads them as int4 (16-byte aligned); then 4 zero
-        # words: the kernel's dynamic work-fetch counter (left zero after every launch)
-        pack = np.concatenate([items.reshape(-1), np.zeros(4, np.int32), meta_np, np.asarray(ids, dtype=np.int32),
+        # work items first: the kernel reads them as int4 (16-byte aligned)
+        pack = np.concatenate([items.reshape(-1), meta_np, np.asarray(ids, dtype=np.int32),
                                valid_np, pos_np, groups.reshape(-1)])
         self._buf = _upload(pack, device)
         o = 0
-        self.work = self._buf[o:o + self.n_work * 8]; o += self.n_work * 8 + 4
+        self.work = self._buf[o:o + self.n_work * 8]; o += self.n_work * 8
         self.meta = self._buf[o:o + meta_np.size]; o += meta_np.size
         self.blk_ids = self._buf[o:o + len(ids)]; o += len(ids)
         self.blk_valid = self._buf[o:o + len(ids)]; o += len(ids)

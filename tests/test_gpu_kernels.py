@@ -219,59 +219,6 @@ def test_prefix_prefill_matches_oracle(hd, hq, hkv, bt, L, reqs, split_kv):
         assert err <= ATTN_ATOL, f"layer {layer}: max |err| {err}"
 
 
-DYN_CASES = ATTN_CASES[:5] + [
-    # > 148 items: CTAs fetch most of their items from the counter
-    (128, 32, 8, 64, 1, [([], [1056])] * 6 + [([512], [544])] * 4),
-]
-
-
-@pytest.mark.parametrize("hd,hq,hkv,bt,L,reqs", DYN_CASES)
-def test_prefix_prefill_dynamic_fetch_matches_oracle(hd, hq, hkv, bt, L, reqs):
-    """RCB_WORK_DYNAMIC plans (items from an atomic counter): same results as the oracle on
-    every launch of the same work list (the last CTA resets the counter), counter left 0."""
-    nb = 600
-    pool = _pool(nb, L, hkv, bt, hd, seed=hd + hq + bt + 1)
-    free = list(np.random.default_rng(bt + 1).permutation(nb))
-    requests = []
-    for prefix, suffix in reqs:
-        blocks, valid = _table(prefix + suffix, bt, free)
-        requests.append((sum(suffix), sum(prefix), blocks, valid))
-    total_q = sum(r[0] for r in requests)
-    g = torch.Generator(device="cuda")
-    g.manual_seed(11)
-    q = torch.randn((total_q, hq, hd), generator=g, device="cuda").to(torch.bfloat16)
-    plan = kernels.AttnPlan(requests, block_tokens=bt, n_q_heads=hq, n_kv_heads=hkv,
-                            dynamic=True)
-    assert plan.dynamic and plan.work_flags & _lib.RCB_WORK_DYNAMIC
-    refs = [attn_oracle.prefix_prefill(q.cpu().float(), pool.cpu(), requests, layer)
-            for layer in range(L)]
-    for rep in range(3):
-        for layer in range(L):
-            out = torch.zeros_like(q)
-            kernels.prefix_prefill(q, out, plan, pool.data_ptr(), nb, block_tokens=bt,
-                                   n_layers=L, n_kv_heads=hkv, head_dim=hd, layer=layer)
-            torch.cuda.synchronize()
-            err = (out.cpu().float() - refs[layer]).abs().max().item()
-            assert err <= ATTN_ATOL, f"launch {rep}, layer {layer}: max |err| {err}"
-    sched = plan._buf[plan.n_work * 8: plan.n_work * 8 + 4].cpu()
-    assert sched.tolist() == [0, 0, 0, 0]
-
-
-def test_attn_plan_picks_dynamic_fetch_for_imbalanced_batches():
-    # the bench's mixed step (misses, partial hits, full hits): static split 1.06 -> dynamic
-    bt = 64
-    reqs, pos = [], 0
-    for a, b in [(0, 1056)] * 26 + [(512, 544)] * 26 + [(1024, 32)] * 12:
-        n = -(-(a + b) // bt)
-        reqs.append((b, a, list(range(pos, pos + n)), [bt] * (n - 1) + [a + b - (n - 1) * bt]))
-        pos += n
-    assert kernels.AttnPlan(reqs, block_tokens=bt, n_q_heads=32, n_kv_heads=8).dynamic
-    # equal items (full hits: 3.5 items per CTA) and one request stay static
-    hits = [(32, 1024, list(range(i * 17, i * 17 + 17)), [64] * 16 + [32]) for i in range(64)]
-    assert not kernels.AttnPlan(hits, block_tokens=bt, n_q_heads=32, n_kv_heads=8).dynamic
-    assert not kernels.AttnPlan(reqs[:1], block_tokens=bt, n_q_heads=32, n_kv_heads=8).dynamic
-
-
 def test_rope_table_must_cover_the_positions():
     pool = torch.zeros((4, 1, 2, 1, 16, 64), dtype=torch.bfloat16, device="cuda")
     kv = torch.zeros((3, 64), dtype=torch.bfloat16, device="cuda")

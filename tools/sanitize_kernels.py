@@ -26,7 +26,7 @@ def table(segs, bt, free):
     return blocks, valid
 
 
-def attention(hq, hkv, hd, bt, shapes, rope, split_kv=False, dynamic=None):
+def attention(hq, hkv, hd, bt, shapes, rope, split_kv=False):
     nb = 64
     g = torch.Generator(device="cuda").manual_seed(hq * hkv + bt)
     pool = torch.randn((nb, 1, 2, hkv, bt, hd), generator=g, device="cuda").to(torch.bfloat16)
@@ -39,8 +39,7 @@ def attention(hq, hkv, hd, bt, shapes, rope, split_kv=False, dynamic=None):
     qkv = torch.randn((T, (hq + 2 * hkv) * hd), generator=g, device="cuda").to(torch.bfloat16)
     q = qkv[:, : hq * hd]
     out = torch.empty((T, hq, hd), dtype=torch.bfloat16, device="cuda")
-    plan = kernels.AttnPlan(reqs, block_tokens=bt, n_q_heads=hq, n_kv_heads=hkv, split_kv=split_kv,
-                            dynamic=dynamic)
+    plan = kernels.AttnPlan(reqs, block_tokens=bt, n_q_heads=hq, n_kv_heads=hkv, split_kv=split_kv)
     tab = kernels.rope_table(max(plan.max_pos, 2) + 1, hd, 1e4) if rope else None
     kernels.prefix_prefill(q if rope else q.contiguous().view(T, hq, hd), out, plan,
                            pool.data_ptr(), nb, block_tokens=bt, n_layers=1, n_kv_heads=hkv,
@@ -66,9 +65,6 @@ def main():
     # MHA with fused RoPE: direct O stores, Q(ii+2) landing right after item ii's last QK
     errs["mha_rope"] = attention(4, 4, 128, 64, [([], [544]), ([128], [300]), ([], [130])],
                                  rope=True)
-    # dynamic work fetch: 272 items on <= 148 CTAs, items from the atomic counter
-    errs["gqa_rope_dynamic"] = attention(32, 8, 128, 64, [([], [1056]), ([], [1000])],
-                                         rope=True, dynamic=True)
     errs["decode"] = attention(32, 8, 128, 64, [([500], [1]), ([300], [1])], rope=True)
     errs["split_kv"] = attention(8, 1, 128, 64, [([1500], [1])], rope=False, split_kv=True)
     # retrieval scan + merge, shard merge

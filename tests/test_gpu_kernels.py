@@ -322,10 +322,13 @@ def test_prefix_prefill_fused_rope_matches_oracle(hd, hq, hkv, bt):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("with_q", [True, False])
-def test_kv_write_rope_table_is_bit_identical(with_q):
-    """rcb_kv_write_rope_table (cos/sin from rcb_rope_table, 8 tokens per CTA) writes the
-    same bytes as the per-token sincosf kernel: both use theta^(-2i/d) via exp2f + sincosf."""
-    hd, hq, hkv, bt, L, nb, T, theta = 128, 32, 8, 64, 2, 96, 203, 1e6
+@pytest.mark.parametrize("hq,hkv", [(32, 8), (32, 32), (40, 40)])
+def test_kv_write_rope_table_is_bit_identical(with_q, hq, hkv):
+    """rcb_kv_write_rope_table (cos/sin from rcb_rope_table; 8, 2 or 1 tokens per CTA as the
+    row width grows: Mistral-7B, LLaMA2-7B, LLaMA2-13B K/V rows, 203 tokens so the last CTA
+    is ragged) writes the same bytes as the per-token sincosf kernel: both use
+    theta^(-2i/d) via exp2f + sincosf."""
+    hd, bt, L, nb, T, theta = 128, 64, 2, 96, 203, 1e6
     g = torch.Generator(device="cuda")
     g.manual_seed(3)
     qkv = torch.randn((T, (hq + 2 * hkv) * hd), generator=g, device="cuda").to(torch.bfloat16)

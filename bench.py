@@ -135,7 +135,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(loaded), "source": "nvml, 5 ms"}
 
 
-NCU_TAG = "r2m"  # profiles/<tag>_ncu_summary.json: captures of the current kernels
+NCU_TAG = "r2o"  # profiles/<tag>_ncu_summary.json: captures of the current kernels
 E2E_WARM = 2  # untimed live steps before the e2e timing
 
 

@@ -123,3 +123,31 @@ def test_live_engine_reproduces_reference_and_golden(path):
     assert report.per_request_csv() == plain.per_request_csv()
     assert json.loads(json.dumps(rec.events)) == g["events"]
     assert report.aggregates()["swap_outs"] == g["aggregates"]["swap_outs"]
+
+
+def test_native_pool_rejects_duplicate_keys_without_mutation():
+    # a key repeated in one swap call would leak blocks and alias a host copy: the C-ABI
+    # rejects the call before touching any state (block_pool.cpp has_duplicate)
+    p = pool_mod.accounting_pool(8, 8, 16)
+    p.node_alloc_gpu(1, 32)
+    gpu_before = p.node_blocks(1, pool_mod.GPU)
+    with pytest.raises(pool_mod.PoolError):
+        p.node_swap_out([1, 1])
+    assert p.node_blocks(1, pool_mod.GPU) == gpu_before
+    p.node_swap_out([1])  # demotes: host copy made, GPU blocks freed
+    host = p.node_blocks(1, pool_mod.HOST)
+    assert len(host) == 2 and p.node_blocks(1, pool_mod.GPU) == []
+    with pytest.raises(pool_mod.PoolError):
+        p.node_swap_in([1, 1])
+    assert p.node_blocks(1, pool_mod.HOST) == host
+    p.node_swap_in([1])
+    assert len(p.node_blocks(1, pool_mod.GPU)) == 2
+
+
+def test_pool_blocks_counts_node_tails_when_any_doc_is_ragged():
+    from paper_2404_12457_b200.workloads import pool_blocks
+    # every doc a multiple of the block: no tail blocks, just ceil(cap/B) + segments + slack
+    assert pool_blocks(10240, 16, [16, 32, 64], 4) == 640 + 4 + 8
+    # one ragged doc (17 tokens): up to cap // min_doc resident nodes may each own a tail block
+    assert pool_blocks(10240, 16, [16, 17, 64], 4) == 640 + 10240 // 16 + 4 + 8
+    assert pool_blocks(0, 16, [17], 4) == 0
